@@ -1,0 +1,174 @@
+/* gpzb.h — C ABI of the B200-native GPZ compress / decompress path.
+ *
+ * The entry points replace the reference package's hot path
+ * (/root/reference/pkg/src/gpz):
+ *
+ *   gpzb_compress        <- pipeline.compress            pipeline.py:73-103
+ *                           (resolve_absolute_bound model.py:183-199,
+ *                            _encode_block pipeline.py:38-70, compact +
+ *                            write_container container.py:203-230)
+ *   gpzb_range           <- model.resolve_absolute_bound model.py:183-199
+ *                           + Dataset finiteness check   model.py:75-77
+ *   gpzb_encode          <- the per-block map + compact  pipeline.py:78-103
+ *   gpzb_parse_header    <- container.read_container     container.py:245-267
+ *   gpzb_decompress      <- pipeline.decompress          pipeline.py:160-205
+ *   gpzb_block_counts    <- (iter_decompressed_blocks support, pipeline.py:208-215)
+ *
+ * Conventions
+ *  - Every device pointer is caller-owned (PyTorch's caching allocator in the
+ *    Python host layer).  The library never allocates or frees device memory
+ *    and keeps no global state; calls are re-entrant.
+ *  - Work is stream-ordered on the caller's cudaStream_t (passed as void*).
+ *    Functions whose name ends in _async return after enqueueing; the others
+ *    synchronise the stream once at the end and read back a small result
+ *    record (one D2H of < 128 bytes).
+ *  - Status codes mirror gpz.errors (errors.py:4-17):
+ *        0 ok, 1 DomainError, 2 WidthOverflow, 3 CorruptData,
+ *        4 unsupported (valid input outside the kernels' envelope),
+ *        5 invalid argument, >= 100 CUDA error.
+ *    gpzb_result.block carries the first failing block (the serial
+ *    first-error semantics of pipeline.py:80-83 and :183-184) or -1 for
+ *    dataset/container-level errors; gpzb_reason_message() gives the text.
+ */
+#ifndef GPZB_H
+#define GPZB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GPZB_OK 0
+#define GPZB_DOMAIN_ERROR 1
+#define GPZB_WIDTH_OVERFLOW 2
+#define GPZB_CORRUPT_DATA 3
+#define GPZB_UNSUPPORTED 4
+#define GPZB_INVALID_ARGUMENT 5
+#define GPZB_CUDA_ERROR 100
+
+#define GPZB_F32 0          /* model.Precision codes (model.py:29-31) */
+#define GPZB_F64 1
+#define GPZB_ABSOLUTE 0     /* model.EbMode codes (model.py:51-53) */
+#define GPZB_RANGE_RELATIVE 1
+
+#define GPZB_GLOBAL_HEADER_SIZE 46   /* "<4sHBBBBddIQQ", container.py:57 */
+#define GPZB_MAX_BLOCK_SIZE 1024     /* kernels: one CTA of 256 threads x 4 particles per block */
+
+typedef struct gpzb_result {
+  int32_t status;          /* GPZB_* class of the error the reference would raise first */
+  int32_t reason;          /* reason code, see gpzb_reason_message */
+  int64_t block;           /* first failing block, -1 if not block-scoped */
+  int32_t axis;            /* axis for per-axis reasons, else -1 */
+  uint32_t nonfinite_mask; /* bit a: axis a holds non-finite values (input or output) */
+  uint64_t out_len;        /* compress: container bytes; decompress: particles */
+  double eb_abs;           /* compress: resolved absolute bound */
+  /* raw decode diagnostics (iter_decompressed_blocks needs them separately) */
+  int64_t decode_block;    /* first block failing a decode check, or -1 */
+  int32_t decode_reason;
+  int32_t decode_axis;
+  int64_t count_block;     /* first block whose particle count breaks the boundary math, or -1 */
+  uint32_t table_flags;    /* bit0 start!=0, bit1 not nondecreasing, bit2 end!=payload */
+  uint32_t pad_;
+  uint64_t path_blocks[6]; /* blocks per sort path (diagnostics) */
+} gpzb_result;
+
+typedef struct gpzb_header {   /* GlobalHeader, container.py:84-95 */
+  uint32_t dims;
+  uint32_t precision;
+  uint32_t preserve_order;
+  uint32_t eb_mode;
+  double eb;
+  double eb_abs;
+  uint32_t block_size;
+  uint32_t version;
+  uint64_t particle_count;
+  uint64_t block_count;
+  uint64_t table_end;    /* 46 + 8 (block_count + 1) */
+  uint64_t payload_len;  /* container length - table_end */
+} gpzb_header;
+
+/* ---- sizing ------------------------------------------------------------- */
+
+/* Upper bound of the container length for `count` particles (the caller
+ * allocates the output with it; the true length comes back in out_len). */
+int gpzb_compress_bound(uint64_t count, int dims, int precision, uint32_t block_size,
+                        uint32_t target_segs_per_axis, int preserve_order, uint64_t* out_bytes);
+
+/* Device workspace needed by gpzb_compress / gpzb_range / gpzb_encode. */
+int gpzb_compress_workspace(uint64_t count, int dims, int precision, uint32_t block_size,
+                            uint64_t* ws_bytes);
+
+/* Device workspace needed by gpzb_decompress for a parsed header. */
+int gpzb_decompress_workspace(const gpzb_header* h, uint64_t* ws_bytes);
+
+/* ---- compression -------------------------------------------------------- */
+
+/* Zero the workspace's result record and look-back state (enqueued). */
+int gpzb_workspace_reset_async(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t block_size,
+                               void* stream);
+
+/* K1: per-block bounds + global joint range + finiteness flags (enqueued).
+ * axes: `dims` device pointers to `count` coordinates each. */
+int gpzb_range_async(const void* const* axes, int dims, int precision, uint64_t count,
+                     uint32_t block_size, void* ws, uint64_t ws_bytes, void* stream);
+
+/* Device address of the two int64 range words inside `ws` (order-preserving
+ * encodings of -lo and +hi; all-reduce them with MAX across ranks to get the
+ * global range of a sharded dataset, see DESIGN.md section multi-GPU). */
+int gpzb_range_words(void* ws, uint64_t ws_bytes, int64_t** words);
+
+/* K2: quantize + sort + encode + decoupled-look-back concatenation (enqueued).
+ * Writes the full container (global header, offset table, payloads) into
+ * `out` (capacity out_cap from gpzb_compress_bound).
+ *   eb_mode == GPZB_RANGE_RELATIVE: eb_abs = eb * span of the range words
+ *   (gpzb_range_async must have run on this ws); else eb_abs = eb.
+ *   table_base / header_count / header_blocks: sharding hooks — payload
+ *   offsets are written as table_base + local prefix, and the global header
+ *   (written when write_header != 0) names header_count particles in
+ *   header_blocks blocks.  Single-GPU callers pass 0, count, ceil(count/bs), 1. */
+int gpzb_encode_async(const void* const* axes, int dims, int precision, uint64_t count, double eb,
+                      int eb_mode, uint32_t block_size, uint32_t target_segs_per_axis,
+                      int preserve_order, void* ws, uint64_t ws_bytes, uint8_t* out,
+                      uint64_t out_cap, uint64_t table_base, uint64_t header_count,
+                      uint64_t header_blocks, int write_header, void* stream);
+
+/* Synchronise `stream` and read the result record of the last encode. */
+int gpzb_compress_result(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t block_size,
+                         void* stream, gpzb_result* res);
+
+/* Convenience: reset + range (REL) + encode + result, one call. */
+int gpzb_compress(const void* const* axes, int dims, int precision, uint64_t count, double eb,
+                  int eb_mode, uint32_t block_size, uint32_t target_segs_per_axis,
+                  int preserve_order, void* ws, uint64_t ws_bytes, uint8_t* out,
+                  uint64_t out_cap, void* stream, gpzb_result* res);
+
+/* ---- decompression ------------------------------------------------------ */
+
+/* Host-side validation of the 46-byte global header against the container
+ * length (read_container's header checks, container.py:249-281). */
+int gpzb_parse_header(const uint8_t* host_bytes, uint64_t avail, uint64_t container_len,
+                      gpzb_header* h, gpzb_result* res);
+
+/* Per-block particle counts read from the block headers (for
+ * iter_decompressed_blocks' exclusive output offsets).  counts: u64[B]. */
+int gpzb_block_counts_async(const uint8_t* container, uint64_t container_len,
+                            const gpzb_header* h, uint64_t* counts, void* stream);
+
+/* K4: table validation, per-block parse + unpack + run expansion +
+ * dequantize, written to axes_out[a][out_offsets ? out_offsets[i] : i*bs + j].
+ * axes_out capacity: out_capacity particles per axis. */
+int gpzb_decompress(const uint8_t* container, uint64_t container_len, const gpzb_header* h,
+                    void* const* axes_out, uint64_t out_capacity, const uint64_t* out_offsets,
+                    void* ws, uint64_t ws_bytes, void* stream, gpzb_result* res);
+
+/* ---- diagnostics -------------------------------------------------------- */
+
+const char* gpzb_reason_message(int reason);
+const char* gpzb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GPZB_H */

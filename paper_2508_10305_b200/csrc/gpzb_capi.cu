@@ -1,0 +1,456 @@
+// C ABI of the GPZ B200 path (declared in include/gpzb.h).
+//
+// Host-side orchestration only: workspace layout, kernel dispatch over
+// (dims, precision, preserve_order), the one small result read-back per call,
+// and the container's global-header validation (container.py:245-281).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "gpzb_decode.cuh"
+#include "gpzb_encode.cuh"
+
+using namespace gpzb;
+
+namespace {
+
+constexpr uint64_t kAlign = 256;
+inline uint64_t align_up(uint64_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
+
+struct EncLayout {
+  uint64_t status, bounds, total;
+};
+
+inline uint64_t nblocks_of(uint64_t count, uint32_t bs) { return bs ? (count + bs - 1) / bs : 0; }
+
+EncLayout enc_layout(uint64_t nblocks, int dims, int prec) {
+  EncLayout L;
+  L.status = align_up(sizeof(DevResult));
+  L.bounds = align_up(L.status + 8 * nblocks);
+  L.total = align_up(L.bounds + nblocks * 2ull * dims * (prec ? 8 : 4));
+  return L;
+}
+
+int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? GPZB_OK : GPZB_CUDA_ERROR + (int)e; }
+
+int check_args(int dims, int prec, uint32_t bs) {
+  if (dims < 1 || dims > 3 || (prec != GPZB_F32 && prec != GPZB_F64)) return GPZB_INVALID_ARGUMENT;
+  if (bs == 0 || bs % 32) return GPZB_INVALID_ARGUMENT;
+  if (bs > (uint32_t)kMaxBs) return GPZB_UNSUPPORTED;
+  return GPZB_OK;
+}
+
+void put_le_host(uint8_t* d, uint64_t v, int n) {
+  for (int i = 0; i < n; ++i) d[i] = (uint8_t)(v >> (8 * i));
+}
+uint64_t get_le_host(const uint8_t* d, int n) {
+  uint64_t v = 0;
+  for (int i = 0; i < n; ++i) v |= (uint64_t)d[i] << (8 * i);
+  return v;
+}
+
+void decode_err(unsigned long long w, int64_t* blk, int32_t* axis, int32_t* reason) {
+  const unsigned long long c = ~w;
+  *blk = (int64_t)(c >> 12);
+  *axis = (int32_t)((c >> 8) & 15);
+  *reason = (int32_t)(c & 255);
+}
+
+int status_of_reason(int r) {
+  switch (r) {
+    case R_NONE: return GPZB_OK;
+    case R_NONFINITE: case R_EB_NOT_POSITIVE: case R_NONFINITE_OUT: return GPZB_DOMAIN_ERROR;
+    case R_AXIS_RANGE: case R_GEOMETRY: return GPZB_WIDTH_OVERFLOW;
+    case R_UNSUPPORTED_BS: case R_BLK_WINDOW: return GPZB_UNSUPPORTED;
+    default: return GPZB_CORRUPT_DATA;
+  }
+}
+
+void clear_result(gpzb_result* r) {
+  memset(r, 0, sizeof(*r));
+  r->block = -1;
+  r->axis = -1;
+  r->decode_block = -1;
+  r->count_block = -1;
+}
+
+template <int D, bool F64>
+void launch_range(const EncParams& P, cudaStream_t s) {
+  const uint64_t grid = std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * 8);
+  k_range<D, typename std::conditional<F64, double, float>::type><<<(unsigned)grid, kThreads, 0, s>>>(P);
+}
+
+template <int D, bool F64>
+void launch_encode(const EncParams& P, bool pres, cudaStream_t s) {
+  if (pres) k_encode<D, F64, true><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
+  else k_encode<D, F64, false><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
+}
+
+template <int D, bool F64>
+void launch_decode(const DecParams& P, bool pres, cudaStream_t s) {
+  if (pres) k_decode<D, F64, true><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
+  else k_decode<D, F64, false><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
+}
+
+#define DISPATCH_DP(dims, prec, FN, ...)                      \
+  do {                                                       \
+    if (prec) {                                              \
+      if (dims == 1) FN<1, true>(__VA_ARGS__);               \
+      else if (dims == 2) FN<2, true>(__VA_ARGS__);          \
+      else FN<3, true>(__VA_ARGS__);                         \
+    } else {                                                 \
+      if (dims == 1) FN<1, false>(__VA_ARGS__);              \
+      else if (dims == 2) FN<2, false>(__VA_ARGS__);         \
+      else FN<3, false>(__VA_ARGS__);                        \
+    }                                                        \
+  } while (0)
+
+EncParams make_enc(const void* const* axes, int dims, int prec, uint64_t count, uint32_t bs,
+                   void* ws) {
+  EncParams P;
+  memset(&P, 0, sizeof(P));
+  const uint64_t nb = nblocks_of(count, bs);
+  const EncLayout L = enc_layout(nb, dims, prec);
+  bool vec = true;
+  for (int a = 0; a < dims; ++a) {
+    P.axes[a] = axes[a];
+    vec = vec && ((reinterpret_cast<uintptr_t>(axes[a]) & 15) == 0);
+  }
+  P.count = count;
+  P.nblocks = nb;
+  P.bs = bs;
+  P.vec = vec ? 1 : 0;
+  P.res = reinterpret_cast<DevResult*>(ws);
+  P.status = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(ws) + L.status);
+  P.bounds = static_cast<uint8_t*>(ws) + L.bounds;
+  return P;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gpzb_version(void) { return "gpzb 0.1 sm_100a"; }
+
+const char* gpzb_reason_message(int r) {
+  switch (r) {
+    case R_NONE: return "ok";
+    case R_NONFINITE: return "contains non-finite coordinates";
+    case R_EB_NOT_POSITIVE: return "absolute bound must be positive";
+    case R_AXIS_RANGE: return "axis range over the bound exceeds 64-bit bin indices";
+    case R_GEOMETRY: return "geometry needs segments x offsets beyond the 64-bit linearization range";
+    case R_SHORT: return "container shorter than the 46-byte global header";
+    case R_MAGIC: return "bad magic at byte 0";
+    case R_VERSION: return "unsupported container version";
+    case R_DIMS: return "dims outside 1..3";
+    case R_ENUM: return "invalid precision or eb_mode code";
+    case R_EB_ABS: return "absolute bound is not a positive real";
+    case R_FLAGS: return "unknown flag bits";
+    case R_TABLE_TRUNC: return "container truncated inside the offset table";
+    case R_TABLE_START: return "offset table must start at 0";
+    case R_TABLE_ORDER: return "offset table is not nondecreasing";
+    case R_TABLE_END: return "offset table end does not match the payload length";
+    case R_BLK_SHORT: return "block payload shorter than its header";
+    case R_BLK_UNIQUE: return "more unique ids than particles";
+    case R_BLK_WIDTH: return "stream width exceeds 64 bits";
+    case R_BLK_NOSEG: return "axis has no segments";
+    case R_BLK_OFFBITS: return "axis offset width exceeds 63 bits";
+    case R_BLK_BOUNDS: return "axis bounds are invalid";
+    case R_BLK_TRUNC: return "block truncated";
+    case R_BLK_TRAILING: return "trailing bytes after block streams";
+    case R_BLK_PAD_DELTA: case R_BLK_PAD_COUNT: case R_BLK_PAD_OFF: case R_BLK_PAD_RANK:
+      return "nonzero padding bits in packed stream";
+    case R_BLK_IDS: return "decoded unique ids are not strictly increasing";
+    case R_BLK_ZERO_RUN: return "decoded run length of zero";
+    case R_BLK_RUN_SUM: return "run lengths do not cover the block's particles";
+    case R_BLK_RUN_MAX: return "run length beyond any block size";
+    case R_BLK_AXIS_RANGE: return "axis range over the bound exceeds 64-bit bin indices";
+    case R_BLK_SEGCOUNT: return "segment count inconsistent with the stored bounds";
+    case R_BLK_SEG_RANGE: return "segment id outside the block geometry";
+    case R_BLK_OFF_RANGE: return "segment offset outside the block geometry";
+    case R_BLK_RANKS: return "rank stream is not a permutation";
+    case R_BLK_COUNT: return "particle count differs from the block boundary math";
+    case R_BLK_TOO_BIG: return "particle count beyond the block size";
+    case R_BLK_WINDOW: return "block payload exceeds the CUDA decoder's 24 KB window (oversized stream widths)";
+    case R_NONFINITE_OUT: return "contains non-finite coordinates";
+    case R_TOTAL: return "blocks decode to a different particle count than the header";
+    case R_UNSUPPORTED_BS: return "block_size above the CUDA kernels' 1024-particle limit";
+    default: return "unknown";
+  }
+}
+
+int gpzb_compress_bound(uint64_t count, int dims, int prec, uint32_t bs, uint32_t target, int pres,
+                        uint64_t* out_bytes) {
+  int st = check_args(dims, prec, bs);
+  if (st) return st;
+  if (target == 0 || (target & (target - 1))) return GPZB_INVALID_ARGUMENT;
+  const uint64_t nb = nblocks_of(count, bs);
+  const int S = prec ? 8 : 4;
+  const uint64_t H = 8 + dims * (2 * S + 5) + (pres ? 4 : 3);
+  // widths: deltas <= 64, counts <= bitlen(bs), offsets <= 64, ranks <= bitlen(bs-1)
+  auto bl = [](uint64_t v) { int b = 0; while (v) { ++b; v >>= 1; } return (uint64_t)b; };
+  const uint64_t per = H + (bs * 64ull + 7) / 8 + (bs * bl(bs) + 7) / 8 + (bs * 64ull + 7) / 8 +
+                       (pres ? (bs * bl(bs - 1) + 7) / 8 : 0);
+  *out_bytes = GPZB_GLOBAL_HEADER_SIZE + 8 * (nb + 1) + nb * per + 16;
+  return GPZB_OK;
+}
+
+int gpzb_compress_workspace(uint64_t count, int dims, int prec, uint32_t bs, uint64_t* ws_bytes) {
+  int st = check_args(dims, prec, bs);
+  if (st) return st;
+  *ws_bytes = enc_layout(nblocks_of(count, bs), dims, prec).total;
+  return GPZB_OK;
+}
+
+int gpzb_decompress_workspace(const gpzb_header* h, uint64_t* ws_bytes) {
+  (void)h;
+  *ws_bytes = align_up(sizeof(DevResult));
+  return GPZB_OK;
+}
+
+int gpzb_workspace_reset_async(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t bs, void* stream) {
+  const uint64_t nb = bs ? nblocks_of(count, bs) : 0;
+  const uint64_t need = align_up(sizeof(DevResult)) + 8 * nb;
+  if (ws_bytes < std::min<uint64_t>(need, ws_bytes) || ws_bytes < align_up(sizeof(DevResult)))
+    return GPZB_INVALID_ARGUMENT;
+  return cuda_status(cudaMemsetAsync(ws, 0, std::min(need, ws_bytes), (cudaStream_t)stream));
+}
+
+int gpzb_range_words(void* ws, uint64_t ws_bytes, int64_t** words) {
+  if (ws_bytes < sizeof(DevResult)) return GPZB_INVALID_ARGUMENT;
+  *words = reinterpret_cast<int64_t*>(&reinterpret_cast<DevResult*>(ws)->range_w[0]);
+  return GPZB_OK;
+}
+
+int gpzb_range_async(const void* const* axes, int dims, int prec, uint64_t count, uint32_t bs, void* ws,
+                     uint64_t ws_bytes, void* stream) {
+  int st = check_args(dims, prec, bs);
+  if (st) return st;
+  const uint64_t nb = nblocks_of(count, bs);
+  if (ws_bytes < enc_layout(nb, dims, prec).total) return GPZB_INVALID_ARGUMENT;
+  if (nb == 0) return GPZB_OK;
+  EncParams P = make_enc(axes, dims, prec, count, bs, ws);
+  DISPATCH_DP(dims, prec, launch_range, P, (cudaStream_t)stream);
+  return cuda_status(cudaGetLastError());
+}
+
+int gpzb_encode_async(const void* const* axes, int dims, int prec, uint64_t count, double eb, int eb_mode,
+                      uint32_t bs, uint32_t target, int pres, void* ws, uint64_t ws_bytes, uint8_t* out,
+                      uint64_t out_cap, uint64_t table_base, uint64_t header_count, uint64_t header_blocks,
+                      int write_header, void* stream) {
+  int st = check_args(dims, prec, bs);
+  if (st) return st;
+  if (target == 0 || (target & (target - 1))) return GPZB_INVALID_ARGUMENT;
+  const uint64_t nb = nblocks_of(count, bs);
+  if (ws_bytes < enc_layout(nb, dims, prec).total) return GPZB_INVALID_ARGUMENT;
+  uint64_t bound = 0;
+  gpzb_compress_bound(count, dims, prec, bs, target, pres, &bound);
+  if (out_cap < bound) return GPZB_INVALID_ARGUMENT;
+  if (nb == 0) return GPZB_OK;
+  EncParams P = make_enc(axes, dims, prec, count, bs, ws);
+  P.target = target;
+  P.eb = eb;
+  P.rel = eb_mode == GPZB_RANGE_RELATIVE;
+  P.eb_mode_code = eb_mode;
+  P.header = write_header ? out : nullptr;
+  P.table0 = out + GPZB_GLOBAL_HEADER_SIZE;
+  P.table = out + GPZB_GLOBAL_HEADER_SIZE + 8;
+  P.payload = out + GPZB_GLOBAL_HEADER_SIZE + 8 * (header_blocks + 1);
+  P.table_base = table_base;
+  P.header_count = header_count;
+  P.header_blocks = header_blocks;
+  DISPATCH_DP(dims, prec, launch_encode, P, pres != 0, (cudaStream_t)stream);
+  return cuda_status(cudaGetLastError());
+}
+
+int gpzb_compress_result(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t bs, void* stream,
+                         gpzb_result* res) {
+  clear_result(res);
+  if (ws_bytes < sizeof(DevResult)) return GPZB_INVALID_ARGUMENT;
+  DevResult R;
+  cudaError_t e = cudaMemcpyAsync(&R, ws, sizeof(R), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return res->status = cuda_status(e);
+  const uint64_t nb = nblocks_of(count, bs);
+  res->nonfinite_mask = R.nonfinite_mask;
+  res->eb_abs = R.eb_abs;
+  memcpy(res->path_blocks, R.path_blocks, sizeof(res->path_blocks));
+  if (R.nonfinite_mask) {  // Dataset construction fails before any block (model.py:75-77)
+    res->status = GPZB_DOMAIN_ERROR;
+    res->reason = R_NONFINITE;
+    res->axis = __builtin_ctz(R.nonfinite_mask);
+    return res->status;
+  }
+  if (R.err_block) {
+    decode_err(R.err_block, &res->block, &res->axis, &res->reason);
+    res->status = status_of_reason(res->reason);
+    return res->status;
+  }
+  res->out_len = GPZB_GLOBAL_HEADER_SIZE + 8 * (nb + 1) + R.total_payload;
+  return GPZB_OK;
+}
+
+int gpzb_compress(const void* const* axes, int dims, int prec, uint64_t count, double eb, int eb_mode,
+                  uint32_t bs, uint32_t target, int pres, void* ws, uint64_t ws_bytes, uint8_t* out,
+                  uint64_t out_cap, void* stream, gpzb_result* res) {
+  clear_result(res);
+  int st = check_args(dims, prec, bs);
+  if (st) return res->status = st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t nb = nblocks_of(count, bs);
+  if (nb == 0) {  // empty dataset: header + one table entry (pipeline.py:75, REL uses raw eb)
+    uint8_t h[GPZB_GLOBAL_HEADER_SIZE + 8];
+    memset(h, 0, sizeof(h));
+    memcpy(h, "GPZ1", 4);
+    put_le_host(h + 4, 1, 2);
+    h[6] = (uint8_t)dims;
+    h[7] = (uint8_t)prec;
+    h[8] = pres ? 1 : 0;
+    h[9] = (uint8_t)eb_mode;
+    uint64_t bits;
+    memcpy(&bits, &eb, 8);
+    put_le_host(h + 10, bits, 8);
+    put_le_host(h + 18, bits, 8);
+    put_le_host(h + 26, bs, 4);
+    if (out_cap < sizeof(h)) return res->status = GPZB_INVALID_ARGUMENT;
+    cudaError_t e = cudaMemcpyAsync(out, h, sizeof(h), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return res->status = cuda_status(e);
+    res->out_len = sizeof(h);
+    res->eb_abs = eb;
+    return GPZB_OK;
+  }
+  st = gpzb_workspace_reset_async(ws, ws_bytes, count, bs, stream);
+  if (!st && eb_mode == GPZB_RANGE_RELATIVE) st = gpzb_range_async(axes, dims, prec, count, bs, ws, ws_bytes, stream);
+  if (!st && eb_mode != GPZB_RANGE_RELATIVE) {
+    // ABS mode still validates finiteness inside K2 (block_bounds)
+  }
+  if (!st)
+    st = gpzb_encode_async(axes, dims, prec, count, eb, eb_mode, bs, target, pres, ws, ws_bytes, out, out_cap,
+                           0, count, nb, 1, stream);
+  if (st) return res->status = st;
+  return gpzb_compress_result(ws, ws_bytes, count, bs, stream, res);
+}
+
+int gpzb_parse_header(const uint8_t* hb, uint64_t avail, uint64_t len, gpzb_header* h, gpzb_result* res) {
+  clear_result(res);
+  memset(h, 0, sizeof(*h));
+  auto fail = [&](int r) { res->status = GPZB_CORRUPT_DATA; res->reason = r; return res->status; };
+  if (len < GPZB_GLOBAL_HEADER_SIZE || avail < GPZB_GLOBAL_HEADER_SIZE) return fail(R_SHORT);
+  if (memcmp(hb, "GPZ1", 4) != 0) return fail(R_MAGIC);
+  h->version = (uint32_t)get_le_host(hb + 4, 2);
+  if (h->version != 1) return fail(R_VERSION);
+  h->dims = hb[6];
+  if (h->dims < 1 || h->dims > 3) return fail(R_DIMS);
+  h->precision = hb[7];
+  const uint32_t flags = hb[8];
+  h->eb_mode = hb[9];
+  if (h->precision > 1 || h->eb_mode > 1) return fail(R_ENUM);
+  uint64_t b = get_le_host(hb + 10, 8);
+  memcpy(&h->eb, &b, 8);
+  b = get_le_host(hb + 18, 8);
+  memcpy(&h->eb_abs, &b, 8);
+  if (!(std::isfinite(h->eb_abs) && h->eb_abs > 0)) return fail(R_EB_ABS);
+  if (flags & ~1u) return fail(R_FLAGS);
+  h->preserve_order = flags & 1;
+  h->block_size = (uint32_t)get_le_host(hb + 26, 4);
+  h->particle_count = get_le_host(hb + 30, 8);
+  h->block_count = get_le_host(hb + 38, 8);
+  const unsigned __int128 te = (unsigned __int128)GPZB_GLOBAL_HEADER_SIZE + ((unsigned __int128)h->block_count + 1) * 8;
+  if ((unsigned __int128)len < te) return fail(R_TABLE_TRUNC);
+  h->table_end = (uint64_t)te;
+  h->payload_len = len - h->table_end;
+  return GPZB_OK;
+}
+
+int gpzb_block_counts_async(const uint8_t* c, uint64_t len, const gpzb_header* h, uint64_t* counts, void* stream) {
+  if (h->block_count == 0) return GPZB_OK;
+  const unsigned grid = (unsigned)((h->block_count + 255) / 256);
+  k_block_counts<<<grid, 256, 0, (cudaStream_t)stream>>>(c, len, h->table_end, h->payload_len, h->block_count,
+                                                          counts);
+  return cuda_status(cudaGetLastError());
+}
+
+int gpzb_decompress(const uint8_t* c, uint64_t len, const gpzb_header* h, void* const* axes_out,
+                    uint64_t out_cap, const uint64_t* out_offsets, void* ws, uint64_t ws_bytes, void* stream,
+                    gpzb_result* res) {
+  clear_result(res);
+  if (ws_bytes < sizeof(DevResult)) return res->status = GPZB_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  DevResult R;
+  memset(&R, 0, sizeof(R));
+  if (h->block_count > 0) {
+    if (h->block_count > 0x7fffffffull) return res->status = GPZB_UNSUPPORTED;
+    cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(DevResult), s);
+    if (e != cudaSuccess) return res->status = cuda_status(e);
+    DecParams P;
+    memset(&P, 0, sizeof(P));
+    P.c = c;
+    P.len = len;
+    P.table_end = h->table_end;
+    P.payload_len = h->payload_len;
+    P.nblocks = h->block_count;
+    P.count = h->particle_count;
+    P.bs = h->block_size;
+    P.eb_abs = h->eb_abs;
+    for (uint32_t a = 0; a < h->dims; ++a) P.out[a] = axes_out[a];
+    P.out_cap = out_cap;
+    P.out_offsets = out_offsets;
+    P.res = reinterpret_cast<DevResult*>(ws);
+    DISPATCH_DP(h->dims, h->precision, launch_decode, P, h->preserve_order != 0, s);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&R, ws, sizeof(R), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return res->status = cuda_status(e);
+  }
+  res->table_flags = R.table_flags;
+  res->nonfinite_mask = R.nonfinite_mask;
+  if (R.err_block) decode_err(R.err_block, &res->decode_block, &res->decode_axis, &res->decode_reason);
+  if (R.err_count) {
+    int32_t ax, rs;
+    decode_err(R.err_count, &res->count_block, &ax, &rs);
+  }
+  // precedence: read_container table checks, then the first failing block,
+  // then Dataset finiteness, then the total count (pipeline.py:160-205)
+  if (R.table_flags) {
+    res->status = GPZB_CORRUPT_DATA;
+    res->reason = (R.table_flags & 1) ? R_TABLE_START : (R.table_flags & 2) ? R_TABLE_ORDER : R_TABLE_END;
+    return res->status;
+  }
+  int64_t fb = -1;
+  if (res->decode_block >= 0) fb = res->decode_block;
+  if (res->count_block >= 0 && (fb < 0 || res->count_block < fb)) fb = res->count_block;
+  if (fb >= 0) {
+    res->block = fb;
+    if (fb == res->decode_block) {
+      res->reason = res->decode_reason;
+      res->axis = res->decode_axis;
+    } else {
+      res->reason = R_BLK_COUNT;
+    }
+    res->status = res->reason == R_UNSUPPORTED_BS || res->reason == R_BLK_WINDOW ? GPZB_UNSUPPORTED
+                                                                                  : GPZB_CORRUPT_DATA;
+    return res->status;
+  }
+  if (R.nonfinite_mask) {
+    res->status = GPZB_DOMAIN_ERROR;
+    res->reason = R_NONFINITE_OUT;
+    res->axis = __builtin_ctz(R.nonfinite_mask);
+    return res->status;
+  }
+  if (h->block_count == 0 && h->particle_count != 0) {
+    res->status = GPZB_CORRUPT_DATA;
+    res->reason = R_TOTAL;
+    return res->status;
+  }
+  res->out_len = h->particle_count;
+  return GPZB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,271 @@
+"""compress / decompress behind the reference's API, on the B200 kernels.
+
+Mirrors ``gpz.pipeline`` (pipeline.py:32-215): same function names,
+arguments, return types, error classes and "block {i}: ..." messages.  All
+numeric work runs in ``_gpzb.so`` (include/gpzb.h) on the current CUDA
+device and stream; this module only moves buffers and maps status codes.
+
+Extra entry points for device-resident data (no host round trip):
+``compress_device(ds_or_axes, cfg) -> torch.uint8 CUDA tensor`` and
+``decompress_device(container_tensor) -> Dataset`` of CUDA tensors.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+import warnings
+from typing import Iterator
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import lib
+from .errors import CorruptData, DomainError, GpzError, WidthOverflow
+from .model import CompressConfig, Dataset, EbMode, Precision
+
+__all__ = [
+    "compress",
+    "decompress",
+    "compress_device",
+    "decompress_device",
+    "iter_block_slices",
+    "iter_decompressed_blocks",
+    "resolve_absolute_bound",
+    "parse_header",
+]
+
+# reason codes used for message shaping (gpzb_common.cuh)
+_R_NONFINITE, _R_NONFINITE_OUT = 1, 60
+
+
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("the GPZ B200 path needs a CUDA device (there is no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+_WS: dict = {}
+
+
+def _workspace(nbytes: int) -> torch.Tensor:
+    """Per-device scratch, grown on demand (the library never allocates)."""
+    dev = _device()
+    buf = _WS.get(dev.index)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=dev)
+        _WS[dev.index] = buf
+    return buf
+
+
+def _check(st: int, res: "_lib.Result | None" = None) -> None:
+    if st == _lib.OK:
+        return
+    if res is None:
+        res = _lib.Result(status=st, reason=0, block=-1, axis=-1)
+    msg = _lib.reason_message(res.reason)
+    where = f"block {res.block}: " if res.block >= 0 else ""
+    if st == _lib.DOMAIN:
+        if res.reason in (_R_NONFINITE, _R_NONFINITE_OUT):
+            raise DomainError(f"axis {res.axis} contains non-finite coordinates")
+        raise DomainError(where + msg)
+    if st == _lib.WIDTH:
+        raise WidthOverflow(f"{where}axis {res.axis}: {msg}" if res.reason == 3 else where + msg)
+    if st == _lib.CORRUPT:
+        if res.axis >= 0 and res.reason in (33, 34, 35, 45, 46):
+            msg = f"axis {res.axis}: {msg}"
+        raise CorruptData(where + msg)
+    if st == _lib.UNSUPPORTED:
+        raise NotImplementedError(msg if res.reason else "configuration outside the CUDA kernels' envelope "
+                                  f"(block_size <= {_lib.MAX_BLOCK_SIZE})")
+    if st == _lib.INVALID:
+        raise ValueError("invalid argument to the GPZ CUDA library")
+    raise RuntimeError(f"CUDA error {st - 100} in the GPZ library")
+
+
+def iter_block_slices(count: int, block_size: int) -> Iterator[slice]:
+    """Storage-order block boundaries; the last block may be partial (pipeline.py:32-35)."""
+    for start in range(0, count, block_size):
+        yield slice(start, min(start + block_size, count))
+
+
+def _as_dataset(ds) -> Dataset:
+    if isinstance(ds, Dataset):
+        return ds
+    return Dataset.from_axes(list(ds))
+
+
+def _device_axes(ds: Dataset) -> list:
+    dev = _device()
+    out = []
+    for a in ds.axes:
+        if isinstance(a, torch.Tensor):
+            t = a if (a.is_cuda and a.device == dev) else a.to(dev, non_blocking=True)
+        else:
+            t = torch.from_numpy(np.ascontiguousarray(a)).to(dev, non_blocking=False)
+        out.append(t.contiguous())
+    return out
+
+
+def compress_device(ds, cfg: CompressConfig) -> torch.Tensor:
+    """Container bytes as a CUDA uint8 tensor (a view of the output buffer)."""
+    ds = _as_dataset(ds)
+    axes = _device_axes(ds)
+    count, dims, prec = ds.count, ds.dims, ds.precision.value
+    bs, t = cfg.block_size, cfg.target_segs_per_axis
+    ws_bytes = ctypes.c_uint64()
+    _check(lib.gpzb_compress_workspace(count, dims, prec, bs, ctypes.byref(ws_bytes)))
+    bound = ctypes.c_uint64()
+    _check(lib.gpzb_compress_bound(count, dims, prec, bs, t, int(cfg.preserve_order), ctypes.byref(bound)))
+    ws = _workspace(ws_bytes.value)
+    out = torch.empty(bound.value, dtype=torch.uint8, device=axes[0].device)
+    res = _lib.Result()
+    st = lib.gpzb_compress(_lib.ptr_array([a.data_ptr() for a in axes]), dims, prec, count,
+                           float(cfg.error_bound), cfg.eb_mode.value, bs, t, int(cfg.preserve_order),
+                           ws.data_ptr(), ws.numel(), out.data_ptr(), bound.value, _stream(), ctypes.byref(res))
+    _check(st, res)
+    compress_device.last_result = res
+    return out[: res.out_len]
+
+
+def compress(ds: Dataset, cfg: CompressConfig, workers: int = 1) -> bytes:
+    """Compress a dataset into container bytes, deterministically (pipeline.py:73-103).
+
+    ``workers`` is accepted for API compatibility; the output never depends
+    on it (pipeline.py:6-7) and the GPU kernels ignore it.
+    """
+    del workers
+    out = compress_device(ds, cfg)
+    return out.cpu().numpy().tobytes()
+
+
+def _host_bytes(data) -> np.ndarray:
+    if isinstance(data, np.ndarray):
+        return np.ascontiguousarray(data.view(np.uint8).reshape(-1))
+    return np.frombuffer(memoryview(data).cast("B"), dtype=np.uint8)
+
+
+def parse_header(head: bytes, container_len: int) -> _lib.Header:
+    """read_container's global-header checks (container.py:245-281), in C."""
+    h = _lib.Header()
+    res = _lib.Result()
+    buf = bytes(head[: _lib.GLOBAL_HEADER_SIZE])
+    st = lib.gpzb_parse_header(buf, len(buf), container_len, ctypes.byref(h), ctypes.byref(res))
+    _check(st, res)
+    return h
+
+
+def _to_device_bytes(data) -> tuple[torch.Tensor, _lib.Header]:
+    if isinstance(data, torch.Tensor):
+        t = data.reshape(-1).view(torch.uint8)
+        if not t.is_cuda:
+            t = t.to(_device(), non_blocking=True)
+        head = t[: _lib.GLOBAL_HEADER_SIZE].cpu().numpy().tobytes()
+        return t, parse_header(head, t.numel())
+    host = _host_bytes(data)
+    h = parse_header(host[: _lib.GLOBAL_HEADER_SIZE].tobytes(), host.size)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        t = torch.from_numpy(host).to(_device())
+    return t, h
+
+
+def _decode(t: torch.Tensor, h: _lib.Header, offsets=None, capacity=None):
+    prec = Precision(h.precision)
+    dev = t.device
+    if capacity is None:
+        capacity = min(h.particle_count, h.block_count * min(h.block_size, _lib.MAX_BLOCK_SIZE))
+    outs = [torch.empty(max(capacity, 1), dtype=prec.torch_dtype, device=dev) for _ in range(h.dims)]
+    ws_bytes = ctypes.c_uint64()
+    _check(lib.gpzb_decompress_workspace(ctypes.byref(h), ctypes.byref(ws_bytes)))
+    ws = _workspace(ws_bytes.value)
+    res = _lib.Result()
+    lib.gpzb_decompress(t.data_ptr(), t.numel(), ctypes.byref(h), _lib.ptr_array([o.data_ptr() for o in outs]),
+                        capacity, offsets.data_ptr() if offsets is not None else None, ws.data_ptr(), ws.numel(),
+                        _stream(), ctypes.byref(res))
+    return outs, res, capacity
+
+
+def decompress_device(data, workers: int = 1) -> Dataset:
+    """Reconstruct on the GPU; the returned Dataset holds CUDA tensors."""
+    del workers
+    t, h = _to_device_bytes(data)
+    outs, res, _ = _decode(t, h)
+    _check(res.status, res)
+    n = h.particle_count
+    return Dataset(axes=tuple(o[:n] for o in outs), precision=Precision(h.precision))
+
+
+def decompress(data, workers: int = 1) -> Dataset:
+    """Reconstruct a dataset from container bytes (pipeline.py:160-205).
+
+    Particles come back in sorted intra-block order unless the container
+    preserves order; block boundaries always match the original.
+    """
+    return decompress_device(data, workers).numpy()
+
+
+def iter_decompressed_blocks(data) -> Iterator[list]:
+    """Per-block reconstructed axes (pipeline.py:208-215): the blocks before
+    the first corrupt one are yielded, then CorruptData("block i: ...")."""
+    t, h = _to_device_bytes(data)
+    if h.block_count == 0:
+        return
+    counts = torch.zeros(h.block_count, dtype=torch.int64, device=t.device)
+    _check(lib.gpzb_block_counts_async(t.data_ptr(), t.numel(), ctypes.byref(h), counts.data_ptr(), _stream()))
+    offsets = torch.zeros_like(counts)
+    offsets[1:] = torch.cumsum(counts, 0)[:-1]
+    capacity = int(counts.sum().item())
+    outs, res, _ = _decode(t, h, offsets, capacity)
+    if res.table_flags:
+        _check(res.status, res)
+    stop = res.decode_block if res.decode_block >= 0 else h.block_count
+    host = [o[:capacity].cpu().numpy() for o in outs]
+    cnt = counts.cpu().numpy()
+    off = offsets.cpu().numpy()
+    for i in range(stop):
+        yield [a[off[i]: off[i] + cnt[i]].copy() for a in host]
+    if res.decode_block >= 0:
+        r = _lib.Result(status=_lib.CORRUPT, reason=res.decode_reason, block=res.decode_block,
+                        axis=res.decode_axis)
+        st = _lib.UNSUPPORTED if res.decode_reason in (53, 70) else _lib.CORRUPT
+        _check(st, r)
+
+
+def _ukey_inv(k: int) -> float:
+    b = (k & 0x7FFFFFFFFFFFFFFF) if (k >> 63) else (~k & 0xFFFFFFFFFFFFFFFF)
+    return struct.unpack("<d", struct.pack("<Q", b))[0]
+
+
+def resolve_absolute_bound(ds: Dataset, cfg: CompressConfig) -> float:
+    """model.resolve_absolute_bound (model.py:183-199); the joint range comes
+    from the range kernel K1 on the GPU."""
+    if cfg.eb_mode is EbMode.ABSOLUTE:
+        return float(cfg.error_bound)
+    ds = _as_dataset(ds)
+    if ds.count == 0:
+        raise DomainError("range-relative bound is undefined for an empty dataset")
+    axes = _device_axes(ds)
+    bs = min(cfg.block_size, _lib.MAX_BLOCK_SIZE)
+    ws_bytes = ctypes.c_uint64()
+    _check(lib.gpzb_compress_workspace(ds.count, ds.dims, ds.precision.value, bs, ctypes.byref(ws_bytes)))
+    ws = _workspace(ws_bytes.value)
+    _check(lib.gpzb_workspace_reset_async(ws.data_ptr(), ws.numel(), ds.count, bs, _stream()))
+    _check(lib.gpzb_range_async(_lib.ptr_array([a.data_ptr() for a in axes]), ds.dims, ds.precision.value,
+                                ds.count, bs, ws.data_ptr(), ws.numel(), _stream()))
+    head = ws[:64].cpu().numpy()
+    nonfinite = int(head[16:20].view(np.uint32)[0])
+    if nonfinite:
+        axis = (nonfinite & -nonfinite).bit_length() - 1
+        raise DomainError(f"axis {axis} contains non-finite coordinates")
+    w0, w1 = (int(v) for v in head[40:56].view(np.uint64))
+    lo, hi = -_ukey_inv(w0), _ukey_inv(w1)
+    span = hi - lo
+    if span <= 0.0:
+        span = 1.0
+    return float(cfg.error_bound) * span

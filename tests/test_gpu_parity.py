@@ -1,0 +1,218 @@
+"""Parity of the CUDA path against the reference (golden fixtures) and the
+CPU oracle, through the public API and the C ABI.  Needs a B200."""
+
+import numpy as np
+import pytest
+import torch
+
+from _golden import CASES, CONTAINERS, GOLDEN, case, case_ids, error_prefix, make_axes, sha
+from oracle import gpz_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+gz = pytest.importorskip("paper_2508_10305_b200")
+
+
+def _cfg(eb, mode, bs, t, pres):
+    return gz.CompressConfig(error_bound=eb, eb_mode=gz.EbMode(mode), block_size=bs, target_segs_per_axis=t,
+                             preserve_order=pres)
+
+
+def _outcome(fn):
+    try:
+        return fn(), None
+    except gz.GpzError as exc:
+        return None, (type(exc).__name__, error_prefix(str(exc)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+@pytest.mark.parametrize("name", case_ids())
+def test_golden_case(name):
+    (_, gen, count, dims, dt, eb, mode, bs, t, pres, seed, extra) = case(name)
+    want = GOLDEN["cases"][name]
+    axes = make_axes(gen, count, dims, dt, seed, extra, O)
+    blob, err = _outcome(lambda: gz.compress(gz.Dataset.from_axes(axes), _cfg(eb, mode, bs, t, pres)))
+    if want["error"]:
+        assert err == (want["error"][0], error_prefix(want["error"][1]))
+        return
+    assert err is None, err
+    assert len(blob) == want["container_len"]
+    if blob != CONTAINERS[name]:
+        ref = CONTAINERS[name]
+        first = next(i for i in range(min(len(ref), len(blob))) if ref[i] != blob[i])
+        raise AssertionError(f"{name}: first differing byte {first} of {len(ref)}")
+    ds = gz.decompress(blob)
+    assert sha(*ds.axes) == want["recon_sha"]
+
+
+def test_device_tensors_and_numpy_give_same_bytes():
+    axes = O.gen_clusters(50_000, dims=3, seed=3)
+    cfg = gz.CompressConfig(error_bound=1e-3)
+    a = gz.compress(gz.Dataset.from_axes(axes), cfg)
+    b = gz.compress(gz.Dataset.from_axes([torch.from_numpy(x).cuda() for x in axes]), cfg)
+    c = gz.compress_device(gz.Dataset.from_axes([torch.from_numpy(x) for x in axes]), cfg)
+    assert a == b == bytes(c.cpu().numpy())
+    assert a == O.compress(axes, O.Config(1e-3))
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_configs_against_oracle(seed):
+    rng = np.random.default_rng(1000 + seed)
+    dims = int(rng.integers(1, 4))
+    dt = np.float32 if rng.random() < 0.7 else np.float64
+    n = int(rng.integers(1, 6000))
+    kind = int(rng.integers(0, 4))
+    if kind == 0:
+        axes = [rng.uniform(-5, 5, n).astype(dt) for _ in range(dims)]
+    elif kind == 1:
+        axes = [(rng.normal(0, 1, n) * 10 ** rng.uniform(-3, 3)).astype(dt) for _ in range(dims)]
+    elif kind == 2:
+        axes = [np.round(rng.uniform(0, 100, n), 1).astype(dt) for _ in range(dims)]
+    else:
+        axes = O.gen_clusters(n, dims=dims, seed=seed, prec=O.F32 if dt == np.float32 else O.F64,
+                              sigma=float(10 ** rng.uniform(-4, -1)))
+    eb = float(10 ** rng.uniform(-7, -1))
+    mode = int(rng.integers(0, 2))
+    bs = int(32 * rng.integers(1, 33))
+    t = int(2 ** rng.integers(0, 8))
+    pres = bool(rng.integers(0, 2))
+    try:
+        want, werr = O.compress(axes, O.Config(eb, mode, bs, t, pres)), None
+    except O.OracleError as exc:
+        want, werr = None, (type(exc).__name__, error_prefix(str(exc)))
+    got, gerr = _outcome(lambda: gz.compress(gz.Dataset.from_axes(axes), _cfg(eb, mode, bs, t, pres)))
+    assert gerr == werr
+    if want is None:
+        return
+    assert got == want
+    rec = gz.decompress(got)
+    for x, y in zip(rec.axes, O.decompress(want)):
+        assert np.array_equal(x, y)
+
+
+def test_bitflip_outcomes_match_reference():
+    g = GOLDEN["bitflip"]
+    base = CONTAINERS["bitflip_base"]
+    bad = []
+    for pos, bit, cls, tag in g["outcomes"]:
+        c = bytearray(base)
+        c[pos] ^= 1 << bit
+        ds, err = _outcome(lambda: gz.decompress(bytes(c)))
+        got = ("ok", sha(*ds.axes)[:16]) if err is None else err
+        if got != (cls, tag):
+            bad.append((pos, bit, got, (cls, tag)))
+    assert not bad, f"{len(bad)} mismatches, first: {bad[:5]}"
+
+
+def test_iter_blocks_matches_decompress_and_oracle():
+    for name in ("clu3_f32_e3", "uni2_f64_pres", "clu3_bs96"):
+        blob = CONTAINERS[name]
+        parts = list(gz.iter_decompressed_blocks(blob))
+        want = list(O.iter_blocks(blob))
+        assert len(parts) == len(want)
+        for p, w in zip(parts, want):
+            for a, b in zip(p, w):
+                assert np.array_equal(a, b)
+
+
+def test_iter_blocks_stops_at_first_corrupt_block():
+    blob = bytearray(CONTAINERS["clu3_bs96"])
+    h = O.read_container(bytes(blob))
+    # corrupt block 3's unique count so it exceeds its particle count
+    start = 46 + 8 * (h[0].blocks + 1) + int(h[1][3])
+    blob[start + 7] ^= 0x40
+    got = []
+    with pytest.raises(gz.CorruptData, match="block 3"):
+        for b in gz.iter_decompressed_blocks(bytes(blob)):
+            got.append(b)
+    assert len(got) == 3
+
+
+def test_million_particle_golden_fixture():
+    big = GOLDEN["big"]
+    axes = O.gen_clusters(1_000_000, dims=3, seed=42)
+    ds = gz.Dataset.from_axes([torch.from_numpy(a).cuda() for a in axes])
+    for eb in (1e-2, 1e-3, 1e-4):
+        blob = gz.compress(ds, gz.CompressConfig(error_bound=eb))
+        want = big[repr(eb)]
+        assert (len(blob), sha(blob)) == (want["container_len"], want["container_sha"])
+        assert sha(*gz.decompress(blob).axes) == want["recon_sha"]
+
+
+def test_resolve_absolute_bound_matches_oracle():
+    axes = O.gen_clusters(100_000, dims=3, seed=5)
+    for mode in (0, 1):
+        cfg = gz.CompressConfig(error_bound=1e-3, eb_mode=gz.EbMode(mode))
+        assert gz.resolve_absolute_bound(gz.Dataset.from_axes(axes), cfg) == \
+            O.absolute_bound(axes, O.Config(1e-3, mode))
+    with pytest.raises(gz.DomainError, match="axis 0"):
+        bad = [a.copy() for a in axes]
+        bad[0][5] = np.inf
+        gz.resolve_absolute_bound(gz.Dataset.from_axes(bad), gz.CompressConfig(error_bound=1e-3))
+
+
+def test_nonfinite_abs_mode_detected_on_device():
+    axes = [np.linspace(0, 1, 5000, dtype=np.float32) for _ in range(3)]
+    axes[2][4000] = np.nan
+    with pytest.raises(gz.DomainError, match="axis 2 contains non-finite"):
+        gz.compress(gz.Dataset.from_axes(axes), gz.CompressConfig(1e-3, eb_mode=gz.EbMode.ABSOLUTE))
+
+
+def test_sort_paths_are_all_exercised():
+    seen = np.zeros(6, np.int64)
+    for name in case_ids():
+        (_, gen, count, dims, dt, eb, mode, bs, t, pres, seed, extra) = case(name)
+        if GOLDEN["cases"][name]["error"] or count == 0:
+            continue
+        axes = make_axes(gen, count, dims, dt, seed, extra, O)
+        gz.compress_device(gz.Dataset.from_axes(axes), _cfg(eb, mode, bs, t, pres))
+        seen += np.array(list(gz.compress_device.last_result.path_blocks))
+    assert (seen[:5] > 0).all(), seen
+
+
+def test_unsupported_block_size_is_loud():
+    with pytest.raises(NotImplementedError):
+        gz.compress(gz.Dataset.from_axes([np.zeros(4096, np.float32)]), gz.CompressConfig(1e-3, block_size=2048))
+
+
+def test_large_sampled_block_parity():
+    """50M particles: sampled blocks of the GPU container against the oracle's
+    per-block encoder, and sampled decoded blocks against its decoder."""
+    n = 50_000_000
+    g = torch.Generator(device="cuda").manual_seed(11)
+    centers = torch.rand(4096, 3, device="cuda", dtype=torch.float64, generator=g)
+    assign = torch.arange(n, device="cuda") // (n // 4096 + 1)
+    pts = centers[assign] + 0.002 * torch.randn(n, 3, device="cuda", dtype=torch.float64, generator=g)
+    axes = [pts[:, a].float().contiguous() for a in range(3)]
+    del pts, assign
+    cfg = gz.CompressConfig(error_bound=1e-3)
+    ds = gz.Dataset.from_axes(axes)
+    c = gz.compress_device(ds, cfg)
+    blob_head = c[:46].cpu().numpy().tobytes()
+    nb = (n + 1023) // 1024
+    table = c[46: 46 + 8 * (nb + 1)].cpu().numpy().view("<u8")
+    pay0 = 46 + 8 * (nb + 1)
+    assert int(table[-1]) + pay0 == c.numel()
+    eb_abs = float(np.frombuffer(blob_head[18:26], "<f8")[0])
+    assert eb_abs == gz.resolve_absolute_bound(ds, cfg)
+    rec = gz.decompress_device(c)
+    rng = np.random.default_rng(0)
+    picks = sorted(set(rng.integers(0, nb, 300).tolist()) | {0, nb - 1})
+    host_c = None
+    for i in picks:
+        sl = slice(i * 1024, min((i + 1) * 1024, n))
+        block = [a[sl].cpu().numpy() for a in axes]
+        want = O.encode_block(block, eb_abs, O.Config(1e-3), O.F32)
+        got = c[pay0 + int(table[i]): pay0 + int(table[i + 1])].cpu().numpy().tobytes()
+        assert got == want, f"block {i}"
+        h = O.Header(3, O.F32, False, 1, 1e-3, eb_abs, 1024, n, nb)
+        dec = O.decode_block(want, h)
+        for a in range(3):
+            assert np.array_equal(rec.axes[a][sl].cpu().numpy(), dec[a]), f"decode block {i}"
+    del host_c
