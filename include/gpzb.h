@@ -155,6 +155,17 @@ int gpzb_parse_header(const uint8_t* host_bytes, uint64_t avail, uint64_t contai
 int gpzb_block_counts_async(const uint8_t* container, uint64_t container_len,
                             const gpzb_header* h, uint64_t* counts, void* stream);
 
+/* K4 enqueued: table validation, per-block parse + unpack + run expansion +
+ * dequantize (see gpzb_decompress); read the outcome with gpzb_decompress_result. */
+int gpzb_decompress_async(const uint8_t* container, uint64_t container_len, const gpzb_header* h,
+                          void* const* axes_out, uint64_t out_capacity, const uint64_t* out_offsets,
+                          void* ws, uint64_t ws_bytes, void* stream);
+
+/* Synchronise `stream` and classify the decode outcome in the reference's
+ * precedence (table checks, first failing block, finiteness, total count). */
+int gpzb_decompress_result(void* ws, uint64_t ws_bytes, const gpzb_header* h, void* stream,
+                           gpzb_result* res);
+
 /* K4: table validation, per-block parse + unpack + run expansion +
  * dequantize, written to axes_out[a][out_offsets ? out_offsets[i] : i*bs + j].
  * axes_out capacity: out_capacity particles per axis. */

@@ -73,6 +73,8 @@ SIGNATURES = {
     "gpzb_parse_header": (_I32, [ctypes.c_char_p, _U64, _U64, _HDR, _RES]),
     "gpzb_block_counts_async": (_I32, [_VP, _U64, _HDR, _VP, _VP]),
     "gpzb_decompress": (_I32, [_VP, _U64, _HDR, ctypes.POINTER(_VP), _U64, _VP, _VP, _U64, _VP, _RES]),
+    "gpzb_decompress_async": (_I32, [_VP, _U64, _HDR, ctypes.POINTER(_VP), _U64, _VP, _VP, _U64, _VP]),
+    "gpzb_decompress_result": (_I32, [_VP, _U64, _HDR, _VP, _RES]),
     "gpzb_reason_message": (ctypes.c_char_p, [_I32]),
     "gpzb_version": (ctypes.c_char_p, []),
 }

@@ -377,38 +377,41 @@ int gpzb_block_counts_async(const uint8_t* c, uint64_t len, const gpzb_header* h
   return cuda_status(cudaGetLastError());
 }
 
-int gpzb_decompress(const uint8_t* c, uint64_t len, const gpzb_header* h, void* const* axes_out,
-                    uint64_t out_cap, const uint64_t* out_offsets, void* ws, uint64_t ws_bytes, void* stream,
-                    gpzb_result* res) {
+int gpzb_decompress_async(const uint8_t* c, uint64_t len, const gpzb_header* h, void* const* axes_out,
+                          uint64_t out_cap, const uint64_t* out_offsets, void* ws, uint64_t ws_bytes,
+                          void* stream) {
+  if (ws_bytes < sizeof(DevResult)) return GPZB_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(DevResult), s);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (h->block_count == 0) return GPZB_OK;
+  if (h->block_count > 0x7fffffffull) return GPZB_UNSUPPORTED;
+  DecParams P;
+  memset(&P, 0, sizeof(P));
+  P.c = c;
+  P.len = len;
+  P.table_end = h->table_end;
+  P.payload_len = h->payload_len;
+  P.nblocks = h->block_count;
+  P.count = h->particle_count;
+  P.bs = h->block_size;
+  P.eb_abs = h->eb_abs;
+  for (uint32_t a = 0; a < h->dims; ++a) P.out[a] = axes_out[a];
+  P.out_cap = out_cap;
+  P.out_offsets = out_offsets;
+  P.res = reinterpret_cast<DevResult*>(ws);
+  DISPATCH_DP(h->dims, h->precision, launch_decode, P, h->preserve_order != 0, s);
+  return cuda_status(cudaGetLastError());
+}
+
+int gpzb_decompress_result(void* ws, uint64_t ws_bytes, const gpzb_header* h, void* stream, gpzb_result* res) {
   clear_result(res);
   if (ws_bytes < sizeof(DevResult)) return res->status = GPZB_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
   DevResult R;
-  memset(&R, 0, sizeof(R));
-  if (h->block_count > 0) {
-    if (h->block_count > 0x7fffffffull) return res->status = GPZB_UNSUPPORTED;
-    cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(DevResult), s);
-    if (e != cudaSuccess) return res->status = cuda_status(e);
-    DecParams P;
-    memset(&P, 0, sizeof(P));
-    P.c = c;
-    P.len = len;
-    P.table_end = h->table_end;
-    P.payload_len = h->payload_len;
-    P.nblocks = h->block_count;
-    P.count = h->particle_count;
-    P.bs = h->block_size;
-    P.eb_abs = h->eb_abs;
-    for (uint32_t a = 0; a < h->dims; ++a) P.out[a] = axes_out[a];
-    P.out_cap = out_cap;
-    P.out_offsets = out_offsets;
-    P.res = reinterpret_cast<DevResult*>(ws);
-    DISPATCH_DP(h->dims, h->precision, launch_decode, P, h->preserve_order != 0, s);
-    e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&R, ws, sizeof(R), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return res->status = cuda_status(e);
-  }
+  cudaError_t e = cudaMemcpyAsync(&R, ws, sizeof(R), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return res->status = cuda_status(e);
   res->table_flags = R.table_flags;
   res->nonfinite_mask = R.nonfinite_mask;
   if (R.err_block) decode_err(R.err_block, &res->decode_block, &res->decode_axis, &res->decode_reason);
@@ -434,8 +437,7 @@ int gpzb_decompress(const uint8_t* c, uint64_t len, const gpzb_header* h, void* 
     } else {
       res->reason = R_BLK_COUNT;
     }
-    res->status = res->reason == R_UNSUPPORTED_BS || res->reason == R_BLK_WINDOW ? GPZB_UNSUPPORTED
-                                                                                  : GPZB_CORRUPT_DATA;
+    res->status = status_of_reason(res->reason);
     return res->status;
   }
   if (R.nonfinite_mask) {
@@ -451,6 +453,15 @@ int gpzb_decompress(const uint8_t* c, uint64_t len, const gpzb_header* h, void* 
   }
   res->out_len = h->particle_count;
   return GPZB_OK;
+}
+
+int gpzb_decompress(const uint8_t* c, uint64_t len, const gpzb_header* h, void* const* axes_out,
+                    uint64_t out_cap, const uint64_t* out_offsets, void* ws, uint64_t ws_bytes, void* stream,
+                    gpzb_result* res) {
+  clear_result(res);
+  int st = gpzb_decompress_async(c, len, h, axes_out, out_cap, out_offsets, ws, ws_bytes, stream);
+  if (st) return res->status = st;
+  return gpzb_decompress_result(ws, ws_bytes, h, stream, res);
 }
 
 }  // extern "C"

@@ -112,25 +112,63 @@ def _device_axes(ds: Dataset) -> list:
     return out
 
 
-def compress_device(ds, cfg: CompressConfig) -> torch.Tensor:
-    """Container bytes as a CUDA uint8 tensor (a view of the output buffer)."""
+def compress_device(ds, cfg: CompressConfig, *, timing=None) -> torch.Tensor:
+    """Container bytes as a CUDA uint8 tensor (a view of the output buffer).
+
+    ``timing``: optional dict; when given, CUDA events are recorded on the
+    current stream around the range kernel (K1) and the encode kernel (K2)
+    and appended to ``timing["range"]`` / ``timing["encode"]`` as pairs.
+    """
     ds = _as_dataset(ds)
     axes = _device_axes(ds)
     count, dims, prec = ds.count, ds.dims, ds.precision.value
-    bs, t = cfg.block_size, cfg.target_segs_per_axis
+    bs, t, pres = cfg.block_size, cfg.target_segs_per_axis, int(cfg.preserve_order)
     ws_bytes = ctypes.c_uint64()
     _check(lib.gpzb_compress_workspace(count, dims, prec, bs, ctypes.byref(ws_bytes)))
     bound = ctypes.c_uint64()
-    _check(lib.gpzb_compress_bound(count, dims, prec, bs, t, int(cfg.preserve_order), ctypes.byref(bound)))
+    _check(lib.gpzb_compress_bound(count, dims, prec, bs, t, pres, ctypes.byref(bound)))
     ws = _workspace(ws_bytes.value)
     out = torch.empty(bound.value, dtype=torch.uint8, device=axes[0].device)
+    ptrs = _lib.ptr_array([a.data_ptr() for a in axes])
     res = _lib.Result()
-    st = lib.gpzb_compress(_lib.ptr_array([a.data_ptr() for a in axes]), dims, prec, count,
-                           float(cfg.error_bound), cfg.eb_mode.value, bs, t, int(cfg.preserve_order),
-                           ws.data_ptr(), ws.numel(), out.data_ptr(), bound.value, _stream(), ctypes.byref(res))
+    stream = _stream()
+    eb, mode = float(cfg.error_bound), cfg.eb_mode.value
+    if count == 0:
+        st = lib.gpzb_compress(ptrs, dims, prec, count, eb, mode, bs, t, pres, ws.data_ptr(), ws.numel(),
+                               out.data_ptr(), bound.value, stream, ctypes.byref(res))
+    else:
+        def ev():
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            return e
+
+        nb = (count + bs - 1) // bs
+        _check(lib.gpzb_workspace_reset_async(ws.data_ptr(), ws.numel(), count, bs, stream))
+        if mode == EbMode.RANGE_RELATIVE.value:
+            e0 = ev() if timing is not None else None
+            _check(lib.gpzb_range_async(ptrs, dims, prec, count, bs, ws.data_ptr(), ws.numel(), stream))
+            if timing is not None:
+                timing.setdefault("range", []).append((e0, ev()))
+        e0 = ev() if timing is not None else None
+        _check(lib.gpzb_encode_async(ptrs, dims, prec, count, eb, mode, bs, t, pres, ws.data_ptr(), ws.numel(),
+                                     out.data_ptr(), bound.value, 0, count, nb, 1, stream))
+        if timing is not None:
+            timing.setdefault("encode", []).append((e0, ev()))
+        st = lib.gpzb_compress_result(ws.data_ptr(), ws.numel(), count, bs, stream, ctypes.byref(res))
     _check(st, res)
     compress_device.last_result = res
     return out[: res.out_len]
+
+
+_PINNED: dict = {}
+
+
+def _pinned(nbytes: int) -> torch.Tensor:
+    buf = _PINNED.get("out")
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+        _PINNED["out"] = buf
+    return buf
 
 
 def compress(ds: Dataset, cfg: CompressConfig, workers: int = 1) -> bytes:
@@ -141,7 +179,9 @@ def compress(ds: Dataset, cfg: CompressConfig, workers: int = 1) -> bytes:
     """
     del workers
     out = compress_device(ds, cfg)
-    return out.cpu().numpy().tobytes()
+    host = _pinned(out.numel())[: out.numel()]
+    host.copy_(out)
+    return host.numpy().tobytes()
 
 
 def _host_bytes(data) -> np.ndarray:
@@ -175,7 +215,7 @@ def _to_device_bytes(data) -> tuple[torch.Tensor, _lib.Header]:
     return t, h
 
 
-def _decode(t: torch.Tensor, h: _lib.Header, offsets=None, capacity=None):
+def _decode(t: torch.Tensor, h: _lib.Header, offsets=None, capacity=None, timing=None):
     prec = Precision(h.precision)
     dev = t.device
     if capacity is None:
@@ -185,17 +225,34 @@ def _decode(t: torch.Tensor, h: _lib.Header, offsets=None, capacity=None):
     _check(lib.gpzb_decompress_workspace(ctypes.byref(h), ctypes.byref(ws_bytes)))
     ws = _workspace(ws_bytes.value)
     res = _lib.Result()
-    lib.gpzb_decompress(t.data_ptr(), t.numel(), ctypes.byref(h), _lib.ptr_array([o.data_ptr() for o in outs]),
-                        capacity, offsets.data_ptr() if offsets is not None else None, ws.data_ptr(), ws.numel(),
-                        _stream(), ctypes.byref(res))
+    stream = _stream()
+    e0 = None
+    if timing is not None:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+    _check(lib.gpzb_decompress_async(t.data_ptr(), t.numel(), ctypes.byref(h),
+                                     _lib.ptr_array([o.data_ptr() for o in outs]), capacity,
+                                     offsets.data_ptr() if offsets is not None else None, ws.data_ptr(),
+                                     ws.numel(), stream))
+    if timing is not None:
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        timing.setdefault("decode", []).append((e0, e1))
+    lib.gpzb_decompress_result(ws.data_ptr(), ws.numel(), ctypes.byref(h), stream, ctypes.byref(res))
     return outs, res, capacity
 
 
-def decompress_device(data, workers: int = 1) -> Dataset:
-    """Reconstruct on the GPU; the returned Dataset holds CUDA tensors."""
+def decompress_device(data, workers: int = 1, *, header=None, timing=None) -> Dataset:
+    """Reconstruct on the GPU; the returned Dataset holds CUDA tensors.
+
+    ``header``: an already parsed header (skips the 46-byte read-back);
+    ``timing``: optional dict receiving CUDA event pairs around K4."""
     del workers
-    t, h = _to_device_bytes(data)
-    outs, res, _ = _decode(t, h)
+    if header is not None and isinstance(data, torch.Tensor) and data.is_cuda:
+        t, h = data, header
+    else:
+        t, h = _to_device_bytes(data)
+    outs, res, _ = _decode(t, h, timing=timing)
     _check(res.status, res)
     n = h.particle_count
     return Dataset(axes=tuple(o[:n] for o in outs), precision=Precision(h.precision))

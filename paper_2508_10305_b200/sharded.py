@@ -1,0 +1,211 @@
+"""Multi-GPU compression by contiguous, block-aligned particle ranges.
+
+One process per GPU (torchrun / torch.distributed, NCCL on the B200 box).
+Blocks are independent, so each rank compresses its own
+range with no data-path collective; the only exchanges are scalars
+(SURVEY.md §8e):
+
+1. REL mode: all-reduce(MAX) of the two order-preserving range words of
+   K1 (encodings of -lo and +hi, model.py:194-195) -> every rank resolves the
+   identical global eb_abs, so its blocks are byte-identical to a
+   single-GPU run over the concatenated dataset;
+2. all-gather of each rank's payload total -> exclusive prefix -> the
+   rank's base offset in the global offset table.
+
+Each rank keeps a *local* container (a valid .gpz of its own blocks); the
+global file is the global header + entry 0 + every rank's table slice
+shifted by its base + every rank's payload, concatenated in rank order
+(`to_global_bytes`).  Shards must be block-aligned: every rank except the
+last holds a multiple of block_size particles.
+
+The orchestration is written against two hooks (`local_range`,
+`local_encode`) so it can be exercised on CPU with the gloo backend in
+tests; the product hooks call the CUDA library.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from ._lib import lib
+from .model import CompressConfig, Dataset, EbMode
+
+_I64_MIN = -(1 << 63)
+
+
+@dataclass
+class ShardedContainer:
+    local: object            # local container (CUDA uint8 tensor, or bytes in CPU tests)
+    rank: int
+    world: int
+    base: int                # this rank's payload offset in the global payload region
+    first_block: int         # global index of this rank's first block
+    global_count: int
+    global_blocks: int
+    local_blocks: int
+    header: bytes            # global 46-byte header (every rank knows it)
+
+    @property
+    def local_bytes(self) -> int:
+        return int(self.local.numel() if hasattr(self.local, "numel") else len(self.local))
+
+
+def _allreduce_max_words(words: torch.Tensor) -> None:
+    """MAX all-reduce of u64 order-preserving words stored as int64."""
+    words ^= _I64_MIN
+    dist.all_reduce(words, op=dist.ReduceOp.MAX)
+    words ^= _I64_MIN
+
+
+def _gather_ints(v: int, device) -> list[int]:
+    t = torch.tensor([v], dtype=torch.int64, device=device)
+    out = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [int(x.item()) for x in out]
+
+
+# ---------------------------------------------------------------- GPU hooks
+class _CudaHooks:
+    def __init__(self, ds: Dataset, cfg: CompressConfig, timing=None):
+        from .pipeline import _check, _device_axes, _stream, _workspace
+
+        self._check, self._stream = _check, _stream
+        self.ds, self.cfg, self.timing = ds, cfg, timing
+        self.axes = _device_axes(ds)
+        self.ptrs = _lib.ptr_array([a.data_ptr() for a in self.axes])
+        n, d, p, bs = ds.count, ds.dims, ds.precision.value, cfg.block_size
+        wsb = ctypes.c_uint64()
+        _check(lib.gpzb_compress_workspace(n, d, p, bs, ctypes.byref(wsb)))
+        self.ws = _workspace(wsb.value)
+        _check(lib.gpzb_workspace_reset_async(self.ws.data_ptr(), self.ws.numel(), n, bs, _stream()))
+
+    def _ev(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def local_range_words(self) -> torch.Tensor:
+        ds, cfg = self.ds, self.cfg
+        e0 = self._ev() if self.timing is not None else None
+        self._check(lib.gpzb_range_async(self.ptrs, ds.dims, ds.precision.value, ds.count, cfg.block_size,
+                                         self.ws.data_ptr(), self.ws.numel(), self._stream()))
+        if self.timing is not None:
+            self.timing.setdefault("range", []).append((e0, self._ev()))
+        return self.ws[40:56].view(torch.int64)  # DevResult.range_w, in place
+
+    def local_encode(self, global_count: int, global_blocks: int):
+        ds, cfg = self.ds, self.cfg
+        bound = ctypes.c_uint64()
+        self._check(lib.gpzb_compress_bound(ds.count, ds.dims, ds.precision.value, cfg.block_size,
+                                            cfg.target_segs_per_axis, int(cfg.preserve_order),
+                                            ctypes.byref(bound)))
+        out = torch.empty(bound.value, dtype=torch.uint8, device=self.axes[0].device)
+        nb = (ds.count + cfg.block_size - 1) // cfg.block_size
+        e0 = self._ev() if self.timing is not None else None
+        self._check(lib.gpzb_encode_async(self.ptrs, ds.dims, ds.precision.value, ds.count,
+                                          float(cfg.error_bound), cfg.eb_mode.value, cfg.block_size,
+                                          cfg.target_segs_per_axis, int(cfg.preserve_order), self.ws.data_ptr(),
+                                          self.ws.numel(), out.data_ptr(), bound.value, 0, ds.count, nb, 1,
+                                          self._stream()))
+        if self.timing is not None:
+            self.timing.setdefault("encode", []).append((e0, self._ev()))
+        res = _lib.Result()
+        st = lib.gpzb_compress_result(self.ws.data_ptr(), self.ws.numel(), ds.count, cfg.block_size,
+                                      self._stream(), ctypes.byref(res))
+        return st, res, out[: res.out_len] if st == 0 else None
+
+
+def _header(dims, prec, cfg: CompressConfig, eb_abs: float, count: int, blocks: int) -> bytes:
+    return struct.pack("<4sHBBBBddIQQ", b"GPZ1", 1, dims, prec, 1 if cfg.preserve_order else 0,
+                       cfg.eb_mode.value, float(cfg.error_bound), eb_abs, cfg.block_size, count, blocks)
+
+
+def compress_device(ds: Dataset, cfg: CompressConfig, *, timing=None, hooks=None) -> ShardedContainer:
+    """Compress this rank's block-aligned shard; collective over the default group."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    bs = cfg.block_size
+    counts = _gather_ints(ds.count, _comm_device())
+    for r in range(world - 1):
+        if counts[r] % bs:
+            raise ValueError(f"rank {r} holds {counts[r]} particles, not a multiple of block_size {bs}")
+    g_count = sum(counts)
+    first_block = sum((c + bs - 1) // bs for c in counts[:rank])
+    g_blocks = sum((c + bs - 1) // bs for c in counts)
+    h = hooks if hooks is not None else _CudaHooks(ds, cfg, timing)
+    if cfg.eb_mode is EbMode.RANGE_RELATIVE:
+        words = h.local_range_words()
+        _allreduce_max_words(words)
+    st, res, local = h.local_encode(g_count, g_blocks)
+    # the first error over ranks in global block order (pipeline.py:80-83);
+    # dataset-level errors (non-finite input) precede every block error
+    inf = 1 << 62
+    key = inf if st == 0 else (-1 if res.block < 0 else first_block + res.block)
+    info = torch.tensor([key, st, res.reason, res.axis], dtype=torch.int64, device=_comm_device())
+    allinfo = [torch.zeros_like(info) for _ in range(world)]
+    dist.all_gather(allinfo, info)
+    win = min(allinfo, key=lambda t: int(t[0]))
+    if int(win[0]) != inf:
+        from .pipeline import _check
+
+        k, wst, wreason, waxis = (int(x) for x in win)
+        _check(wst, _lib.Result(status=wst, reason=wreason, block=k, axis=waxis))
+    nb = (ds.count + bs - 1) // bs
+    payload = int(local.numel() if hasattr(local, "numel") else len(local)) - 46 - 8 * (nb + 1)
+    totals = _gather_ints(payload, _comm_device())
+    base = sum(totals[:rank])
+    header = _header(ds.dims, ds.precision.value, cfg, float(res.eb_abs), g_count, g_blocks)
+    return ShardedContainer(local=local, rank=rank, world=world, base=base, first_block=first_block,
+                            global_count=g_count, global_blocks=g_blocks, local_blocks=nb, header=header)
+
+
+def _comm_device():
+    if dist.get_backend() == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def decompress_device(sc: ShardedContainer, *, timing=None):
+    """Each rank decodes its own blocks (no exchange)."""
+    from .pipeline import decompress_device as dd
+
+    return dd(sc.local, timing=timing)
+
+
+def global_pieces(sc: ShardedContainer) -> tuple[int, bytes, int, bytes]:
+    """(table offset, table bytes, payload offset, payload bytes) of this rank's
+    slice of the global file; rank 0's table slice starts with entry 0."""
+    local = sc.local.cpu().numpy().tobytes() if hasattr(sc.local, "cpu") else bytes(sc.local)
+    nb = sc.local_blocks
+    table = np.frombuffer(local, "<u8", count=nb + 1, offset=46).astype(np.uint64) + np.uint64(sc.base)
+    payload = local[46 + 8 * (nb + 1):]
+    t_off = 46 + 8 * (sc.first_block + 1)
+    p_off = 46 + 8 * (sc.global_blocks + 1) + sc.base
+    tbytes = table[1:].astype("<u8").tobytes()
+    if sc.rank == 0:
+        t_off -= 8
+        tbytes = table[:1].astype("<u8").tobytes() + tbytes
+    return t_off, tbytes, p_off, payload
+
+
+def to_global_bytes(sc: ShardedContainer) -> bytes | None:
+    """Gather every rank's pieces to rank 0 and return the single-file
+    container there (None on other ranks).  Outside any timed region."""
+    pieces = global_pieces(sc)
+    gathered = [None] * sc.world
+    dist.all_gather_object(gathered, pieces)
+    if sc.rank != 0:
+        return None
+    total = max(p_off + len(p) for _, _, p_off, p in gathered)
+    buf = bytearray(total)
+    buf[:46] = sc.header
+    for t_off, t, p_off, p in gathered:
+        buf[t_off:t_off + len(t)] = t
+        buf[p_off:p_off + len(p)] = p
+    return bytes(buf)

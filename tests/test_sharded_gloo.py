@@ -1,0 +1,128 @@
+"""Multi-process (world_size 2, gloo, CPU) test of the sharded orchestration:
+range all-reduce, error agreement, payload-total all-gather and the global
+file assembly.  The per-rank encoder is the oracle here (test-only hooks);
+on the GPU box the same orchestration drives the CUDA kernels."""
+
+import os
+import socket
+import struct
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import gpz_oracle as O
+
+MASK = (1 << 64) - 1
+
+
+def _ukey(v: float) -> int:
+    b = struct.unpack("<Q", struct.pack("<d", v))[0]
+    k = (~b & MASK) if (b >> 63) else (b | (1 << 63))
+    return k - (1 << 64) if k >= (1 << 63) else k
+
+
+def _ukey_inv(k: int) -> float:
+    k &= MASK
+    b = (k & 0x7FFFFFFFFFFFFFFF) if (k >> 63) else (~k & MASK)
+    return struct.unpack("<d", struct.pack("<Q", b))[0]
+
+
+class OracleHooks:
+    """Stand-in for the CUDA hooks: same contract, oracle arithmetic."""
+
+    def __init__(self, axes, cfg):
+        self.axes, self.cfg = axes, cfg
+
+    def local_range_words(self):
+        lo = min(float(a.min()) for a in self.axes)
+        hi = max(float(a.max()) for a in self.axes)
+        self.words = torch.tensor([_ukey(-lo), _ukey(hi)], dtype=torch.int64)
+        return self.words
+
+    def local_encode(self, g_count, g_blocks):
+        import paper_2508_10305_b200._lib as L
+
+        c = self.cfg
+        if c.eb_mode.value == O.RANGE_RELATIVE:
+            lo, hi = -_ukey_inv(int(self.words[0])), _ukey_inv(int(self.words[1]))
+            span = hi - lo
+            eb_abs = c.error_bound * (span if span > 0 else 1.0)
+        else:
+            eb_abs = c.error_bound
+        oc = O.Config(c.error_bound, c.eb_mode.value, c.block_size, c.target_segs_per_axis, c.preserve_order)
+        n = self.axes[0].size
+        pay = []
+        for i, s in enumerate(range(0, n, c.block_size)):
+            try:
+                pay.append(O.encode_block([a[s:s + c.block_size] for a in self.axes], eb_abs, oc, O.F32))
+            except O.OracleError as exc:
+                st = L.WIDTH if isinstance(exc, O.WidthOverflow) else L.DOMAIN
+                return st, L.Result(status=st, reason=3, block=i, axis=0), None
+        n_blk = len(pay)
+        blob = O.assemble(len(self.axes), O.F32, oc, eb_abs, n, pay)
+        assert n_blk == (n + c.block_size - 1) // c.block_size
+        return 0, L.Result(status=0, eb_abs=eb_abs), blob
+
+
+def _run(rank, world, port, case, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2508_10305_b200 as gz
+        from paper_2508_10305_b200 import sharded
+
+        full = O.gen_clusters(5000, dims=3, seed=11)
+        if case == "overflow":
+            full[0] = full[0].astype(np.float32)
+            full[0][3500] = 3e38  # block 3 (rank 1's first block) overflows in ABS mode
+        cuts = [0, 3072, 5000]
+        local = [a[cuts[rank]:cuts[rank + 1]] for a in full]
+        mode = gz.EbMode.ABSOLUTE if case == "overflow" else gz.EbMode.RANGE_RELATIVE
+        cfg = gz.CompressConfig(error_bound=1e-3 if case != "overflow" else 1e-6, eb_mode=mode)
+        ds = gz.Dataset.from_axes(local)
+        try:
+            sc = sharded.compress_device(ds, cfg, hooks=OracleHooks(local, cfg))
+        except gz.GpzError as exc:
+            q.put((rank, "err", type(exc).__name__, str(exc)))
+            return
+        blob = sharded.to_global_bytes(sc)
+        if rank == 0:
+            want = O.compress(full, O.Config(cfg.error_bound, mode.value))
+            q.put((rank, "ok", blob == want, len(want)))
+        else:
+            q.put((rank, "ok", True, 0))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("case", ["rel", "overflow"])
+def test_sharded_global_container_equals_single_process(case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_run, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    out.sort()
+    if case == "rel":
+        assert out[0][1:3] == ("ok", True), out
+        assert out[1][1] == "ok"
+    else:
+        # both ranks raise the same first error, with the global block index
+        for r in out:
+            assert r[1] == "err" and r[2] == "WidthOverflow" and r[3].startswith("block 3"), out
