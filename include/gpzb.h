@@ -118,26 +118,36 @@ int gpzb_range_async(const void* const* axes, int dims, int precision, uint64_t 
  * global range of a sharded dataset, see DESIGN.md section multi-GPU). */
 int gpzb_range_words(void* ws, uint64_t ws_bytes, int64_t** words);
 
-/* K2: quantize + sort + encode + decoupled-look-back concatenation (enqueued).
- * Writes the full container (global header, offset table, payloads) into
- * `out` (capacity out_cap from gpzb_compress_bound).
- *   eb_mode == GPZB_RANGE_RELATIVE: eb_abs = eb * span of the range words
- *   (gpzb_range_async must have run on this ws); else eb_abs = eb.
- *   table_base / header_count / header_blocks: sharding hooks — payload
- *   offsets are written as table_base + local prefix, and the global header
- *   (written when write_header != 0) names header_count particles in
- *   header_blocks blocks.  Single-GPU callers pass 0, count, ceil(count/bs), 1. */
+/* K1.5: per-block geometry records (enqueued, after gpzb_range_async, which
+ * runs in both eb modes because it also produces the per-block bounds).
+ * Routes each block to the 32-bit fast encoder or the general one. */
+int gpzb_encode_plan_async(const void* const* axes, int dims, int precision, uint64_t count, double eb,
+                           int eb_mode, uint32_t block_size, uint32_t target_segs_per_axis,
+                           int preserve_order, void* ws, uint64_t ws_bytes, void* stream);
+
+/* Synchronise and read how many bytes of side buffer the general-encoder
+ * blocks need (0 when every block takes the fast path). */
+int gpzb_encode_side_bytes(void* ws, uint64_t ws_bytes, void* stream, uint64_t* side_bytes);
+
+/* K2w (general blocks, into `side`) + K2 (fast blocks, decoupled look-back,
+ * container assembly), enqueued.  Writes the full container (global header,
+ * offset table, payloads) into `out` (capacity from gpzb_compress_bound).
+ *   table_base / header_count / header_blocks: sharding hooks — table entries
+ *   are written as table_base + local prefix, and the global header (written
+ *   when write_header != 0) names header_count particles in header_blocks
+ *   blocks.  Single-GPU callers pass 0, count, ceil(count/bs), 1. */
 int gpzb_encode_async(const void* const* axes, int dims, int precision, uint64_t count, double eb,
                       int eb_mode, uint32_t block_size, uint32_t target_segs_per_axis,
-                      int preserve_order, void* ws, uint64_t ws_bytes, uint8_t* out,
-                      uint64_t out_cap, uint64_t table_base, uint64_t header_count,
-                      uint64_t header_blocks, int write_header, void* stream);
+                      int preserve_order, void* ws, uint64_t ws_bytes, uint8_t* side,
+                      uint64_t side_bytes, uint8_t* out, uint64_t out_cap, uint64_t table_base,
+                      uint64_t header_count, uint64_t header_blocks, int write_header, void* stream);
 
 /* Synchronise `stream` and read the result record of the last encode. */
 int gpzb_compress_result(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t block_size,
                          void* stream, gpzb_result* res);
 
-/* Convenience: reset + range (REL) + encode + result, one call. */
+/* Convenience: reset + range + plan + encode + result, one call (allocates
+ * the side buffer with cudaMallocAsync when general-path blocks exist). */
 int gpzb_compress(const void* const* axes, int dims, int precision, uint64_t count, double eb,
                   int eb_mode, uint32_t block_size, uint32_t target_segs_per_axis,
                   int preserve_order, void* ws, uint64_t ws_bytes, uint8_t* out,

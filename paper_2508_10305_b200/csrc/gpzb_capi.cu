@@ -9,6 +9,8 @@
 
 #include "gpzb_decode.cuh"
 #include "gpzb_encode.cuh"
+#include "gpzb_encode_narrow.cuh"
+#include "gpzb_encode_wide.cuh"
 
 using namespace gpzb;
 
@@ -18,7 +20,7 @@ constexpr uint64_t kAlign = 256;
 inline uint64_t align_up(uint64_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
 
 struct EncLayout {
-  uint64_t status, bounds, total;
+  uint64_t status, bounds, rec, list, total;
 };
 
 inline uint64_t nblocks_of(uint64_t count, uint32_t bs) { return bs ? (count + bs - 1) / bs : 0; }
@@ -27,7 +29,9 @@ EncLayout enc_layout(uint64_t nblocks, int dims, int prec) {
   EncLayout L;
   L.status = align_up(sizeof(DevResult));
   L.bounds = align_up(L.status + 8 * nblocks);
-  L.total = align_up(L.bounds + nblocks * 2ull * dims * (prec ? 8 : 4));
+  L.rec = align_up(L.bounds + nblocks * 2ull * dims * (prec ? 8 : 4));
+  L.list = align_up(L.rec + nblocks * sizeof(BlkRec));
+  L.total = align_up(L.list + 4 * nblocks);
   return L;
 }
 
@@ -87,9 +91,19 @@ void launch_range(const EncParams& P, cudaStream_t s) {
 }
 
 template <int D, bool F64>
-void launch_encode(const EncParams& P, bool pres, cudaStream_t s) {
-  if (pres) k_encode<D, F64, true><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
-  else k_encode<D, F64, false><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
+void launch_geometry(const EncParams& P, cudaStream_t s) {
+  k_geometry<D, typename std::conditional<F64, double, float>::type>
+      <<<(unsigned)((P.nblocks + 255) / 256), 256, 0, s>>>(P);
+}
+
+template <int D, bool F64>
+void launch_encode(const EncParams& P, bool wide, cudaStream_t s) {
+  if (wide) {
+    const unsigned grid = (unsigned)std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * 4);
+    if (P.preserve) k_encode_wide<D, F64, true><<<grid, kThreads, 0, s>>>(P);
+    else k_encode_wide<D, F64, false><<<grid, kThreads, 0, s>>>(P);
+  }
+  k_encode<D, F64><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
 }
 
 template <int D, bool F64>
@@ -129,6 +143,8 @@ EncParams make_enc(const void* const* axes, int dims, int prec, uint64_t count, 
   P.res = reinterpret_cast<DevResult*>(ws);
   P.status = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(ws) + L.status);
   P.bounds = static_cast<uint8_t*>(ws) + L.bounds;
+  P.rec = reinterpret_cast<BlkRec*>(static_cast<uint8_t*>(ws) + L.rec);
+  P.wide_list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + L.list);
   return P;
 }
 
@@ -240,10 +256,37 @@ int gpzb_range_async(const void* const* axes, int dims, int prec, uint64_t count
   return cuda_status(cudaGetLastError());
 }
 
+int gpzb_encode_plan_async(const void* const* axes, int dims, int prec, uint64_t count, double eb, int eb_mode,
+                           uint32_t bs, uint32_t target, int pres, void* ws, uint64_t ws_bytes, void* stream) {
+  int st = check_args(dims, prec, bs);
+  if (st) return st;
+  if (target == 0 || (target & (target - 1))) return GPZB_INVALID_ARGUMENT;
+  const uint64_t nb = nblocks_of(count, bs);
+  if (ws_bytes < enc_layout(nb, dims, prec).total) return GPZB_INVALID_ARGUMENT;
+  if (nb == 0) return GPZB_OK;
+  EncParams P = make_enc(axes, dims, prec, count, bs, ws);
+  P.target = target;
+  P.eb = eb;
+  P.rel = eb_mode == GPZB_RANGE_RELATIVE;
+  P.preserve = pres != 0;
+  DISPATCH_DP(dims, prec, launch_geometry, P, (cudaStream_t)stream);
+  return cuda_status(cudaGetLastError());
+}
+
+int gpzb_encode_side_bytes(void* ws, uint64_t ws_bytes, void* stream, uint64_t* side_bytes) {
+  if (ws_bytes < sizeof(DevResult)) return GPZB_INVALID_ARGUMENT;
+  unsigned long long v = 0;
+  cudaError_t e = cudaMemcpyAsync(&v, &reinterpret_cast<DevResult*>(ws)->side_bytes, 8, cudaMemcpyDeviceToHost,
+                                  (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  *side_bytes = v;
+  return cuda_status(e);
+}
+
 int gpzb_encode_async(const void* const* axes, int dims, int prec, uint64_t count, double eb, int eb_mode,
-                      uint32_t bs, uint32_t target, int pres, void* ws, uint64_t ws_bytes, uint8_t* out,
-                      uint64_t out_cap, uint64_t table_base, uint64_t header_count, uint64_t header_blocks,
-                      int write_header, void* stream) {
+                      uint32_t bs, uint32_t target, int pres, void* ws, uint64_t ws_bytes, uint8_t* side,
+                      uint64_t side_bytes, uint8_t* out, uint64_t out_cap, uint64_t table_base,
+                      uint64_t header_count, uint64_t header_blocks, int write_header, void* stream) {
   int st = check_args(dims, prec, bs);
   if (st) return st;
   if (target == 0 || (target & (target - 1))) return GPZB_INVALID_ARGUMENT;
@@ -258,14 +301,16 @@ int gpzb_encode_async(const void* const* axes, int dims, int prec, uint64_t coun
   P.eb = eb;
   P.rel = eb_mode == GPZB_RANGE_RELATIVE;
   P.eb_mode_code = eb_mode;
+  P.preserve = pres != 0;
+  P.side = side;
   P.header = write_header ? out : nullptr;
   P.table0 = out + GPZB_GLOBAL_HEADER_SIZE;
   P.table = out + GPZB_GLOBAL_HEADER_SIZE + 8;
-  P.payload = out + GPZB_GLOBAL_HEADER_SIZE + 8 * (header_blocks + 1);
+  P.payload = out + GPZB_GLOBAL_HEADER_SIZE + 8 * (nb + 1);
   P.table_base = table_base;
   P.header_count = header_count;
   P.header_blocks = header_blocks;
-  DISPATCH_DP(dims, prec, launch_encode, P, pres != 0, (cudaStream_t)stream);
+  DISPATCH_DP(dims, prec, launch_encode, P, side_bytes > 0, (cudaStream_t)stream);
   return cuda_status(cudaGetLastError());
 }
 
@@ -327,13 +372,19 @@ int gpzb_compress(const void* const* axes, int dims, int prec, uint64_t count, d
     return GPZB_OK;
   }
   st = gpzb_workspace_reset_async(ws, ws_bytes, count, bs, stream);
-  if (!st && eb_mode == GPZB_RANGE_RELATIVE) st = gpzb_range_async(axes, dims, prec, count, bs, ws, ws_bytes, stream);
-  if (!st && eb_mode != GPZB_RANGE_RELATIVE) {
-    // ABS mode still validates finiteness inside K2 (block_bounds)
+  if (!st) st = gpzb_range_async(axes, dims, prec, count, bs, ws, ws_bytes, stream);
+  if (!st) st = gpzb_encode_plan_async(axes, dims, prec, count, eb, eb_mode, bs, target, pres, ws, ws_bytes, stream);
+  uint64_t side_bytes = 0;
+  if (!st) st = gpzb_encode_side_bytes(ws, ws_bytes, stream, &side_bytes);
+  void* side = nullptr;
+  if (!st && side_bytes) {  // the one allocation of the convenience wrapper (stream-ordered pool)
+    cudaError_t e = cudaMallocAsync(&side, side_bytes, s);
+    if (e != cudaSuccess) st = cuda_status(e);
   }
   if (!st)
-    st = gpzb_encode_async(axes, dims, prec, count, eb, eb_mode, bs, target, pres, ws, ws_bytes, out, out_cap,
-                           0, count, nb, 1, stream);
+    st = gpzb_encode_async(axes, dims, prec, count, eb, eb_mode, bs, target, pres, ws, ws_bytes,
+                           static_cast<uint8_t*>(side), side_bytes, out, out_cap, 0, count, nb, 1, stream);
+  if (side) cudaFreeAsync(side, s);
   if (st) return res->status = st;
   return gpzb_compress_result(ws, ws_bytes, count, bs, stream, res);
 }

@@ -57,7 +57,9 @@ struct DevResult {
   unsigned long long range_w[2];    // ukey(-lo), ukey(hi): joint range (model.py:194-195)
   double eb_abs;
   unsigned long long path_blocks[6];
-  unsigned long long pad[2];
+  unsigned long long side_bytes;    // K1.5: bytes reserved in the side buffer for wide blocks
+  unsigned int wide_count;          // K1.5: number of wide blocks
+  unsigned int pad_;
 };
 static_assert(sizeof(DevResult) % 16 == 0, "DevResult alignment");
 

@@ -1,11 +1,15 @@
 // K1 (range) and K2 (fused encode) for the GPZ B200 compressor.
 //
-// K2 runs one CTA (256 threads x 4 particles) per GPZ block and does all
-// four stages of the reference's _encode_block (pipeline.py:38-70) plus the
-// compact step (container.py:203-208) in a single pass:
-//   load -> bounds -> geometry -> quantize -> counting sort (bitmap ranks,
-//   smem atomics) -> RLE/delta/width -> payload size -> decoupled look-back
-//   -> bit-pack into a 16B-realigned smem stage -> vector stores.
+// Pipeline (all stream-ordered, one D2H of 8 bytes between K1.5 and K2):
+//   K1   k_range     per-block bounds, joint range (REL), finiteness
+//   K1.5 k_geometry  per-block geometry record; routes each block to the
+//                    32-bit fast encoder ("narrow") or the general one ("wide")
+//   K2w  k_encode_wide   general encoder (any width, preserve_order) into a
+//                        side buffer, only for the wide blocks
+//   K2   k_encode    narrow blocks: fused quantize -> bitmap counting sort ->
+//                    RLE/delta/width -> size -> decoupled look-back (overlapped
+//                    with bit-packing) -> realigned vector stores; wide blocks:
+//                    look-back + copy of the staged payload.
 #pragma once
 
 #include <type_traits>
@@ -13,6 +17,8 @@
 #include "gpzb_common.cuh"
 
 namespace gpzb {
+
+struct BlkRec;
 
 struct EncParams {
   const void* axes[3];
@@ -33,6 +39,10 @@ struct EncParams {
   uint64_t table_base;     // added to every table entry
   uint64_t header_count, header_blocks;
   int eb_mode_code;
+  int preserve;
+  BlkRec* rec;             // per-block geometry records (K1.5)
+  uint32_t* wide_list;     // blocks routed to the general encoder
+  uint8_t* side;           // staging for the general encoder's payloads
 };
 
 // ----------------------------------------------------------------- loads
@@ -176,38 +186,113 @@ __global__ void __launch_bounds__(kThreads) k_range(const EncParams P) {
   if ((threadIdx.x & 31) == 0 && nf_all) atomicOr(&P.res->nonfinite_mask, nf_all);
 }
 
-// ------------------------------------------------------------------- K2
-struct EncSmem {
-  uint64_t blk;
-  uint64_t excl;
-  AxisGeo geo[3];
-  int ax_err[3];
-  int pad_;
-  __align__(16) double redd[3 * 2 * kWarps];
-  uint32_t red[kWarps * 8];
-  uint32_t scan32[kWarps];
-  unsigned long long scan64[kWarps];
-  __align__(16) uint32_t cnt[kMaxBs];   // run length per distinct segment rank
-  __align__(16) uint64_t uniq[kMaxBs];  // unique segment ids (increasing)
-  union U {
-    struct { uint32_t bm[2048]; uint16_t wp[2048]; } a;  // pass A: segment bitmap
-    struct {
-      uint32_t bm[2048]; uint16_t wp[2048]; uint32_t cnt2[kMaxBs];
-    } b;                                                  // pass B: (rank, offset) bitmap
-    struct { uint16_t segstart[kMaxBs]; uint64_t tmp[kMaxBs]; } c;  // in-group compare
-    struct {
-      uint64_t off[kMaxBs]; uint16_t sr[kMaxBs]; uint16_t rk[kMaxBs]; uint32_t bm[2048]; uint16_t wp[2048];
-    } l;                                                  // LSD on (rank, offset)
-    struct {
-      uint64_t off[kMaxBs]; uint64_t seg[kMaxBs]; uint16_t rk[kMaxBs]; uint32_t bm[1024]; uint16_t wp[1024];
-    } g;                                                  // LSD on (segment, offset)
-    uint32_t stage[6144];                                 // payload staging (24 KB)
-  };
-  __align__(16) U u;
-};
 
-// Bitmap rank machinery shared by every pass: zero / set / prefix.
-// Words [0, nw) of bm, prefix counts into wp.  Returns the number of set bits.
+// ------------------------------------------------------------------ K1.5
+// Per-block geometry record: everything the 32-bit encoder needs, so K2
+// never runs the float64 geometry (one thread per block here instead of a
+// serial phase inside every K2 CTA).
+struct __align__(16) BlkRec {
+  double lo[3];       // block minimum per axis (exact)
+  double rinv[3];     // RN(1/w), certified-reciprocal quantizer
+  double w[3];        // bin width 2*eb_int (exact-division fallback)
+  uint32_t N[3];      // segments per axis
+  uint32_t PN;        // Π N (narrow blocks: <= 65536)
+  uint64_t side_off;  // wide blocks: byte offset of the staged payload
+  uint32_t side_len;  // wide blocks: payload length (written by K2w)
+  uint8_t b[3];       // log2(m) per axis
+  uint8_t sumb;       // Σ log2(m)
+  uint8_t kind;       // 0 narrow, 1 wide, 2 error
+  uint8_t pad[23];
+};
+static_assert(sizeof(BlkRec) == 128, "BlkRec layout");
+
+enum : uint8_t { KIND_NARROW = 0, KIND_WIDE = 1, KIND_ERROR = 2 };
+
+// Largest payload a block can produce given its geometry (stream widths are
+// bounded by bitlen(ΠN - 1), bitlen(n), Σb and bitlen(n - 1)).
+__host__ __device__ inline uint64_t payload_bound(int D, int S, bool pres, uint32_t n, uint32_t wdel_max,
+                                                  uint32_t sumb) {
+  uint32_t wc = 0, wr = 0;
+  for (uint32_t v = n; v; v >>= 1) ++wc;
+  for (uint32_t v = n ? n - 1 : 0; v; v >>= 1) ++wr;
+  const uint64_t H = 8 + D * (2 * S + 5) + (pres ? 4 : 3);
+  return H + (((uint64_t)n * wdel_max + 7) >> 3) + (((uint64_t)n * wc + 7) >> 3) +
+         (((uint64_t)n * sumb + 7) >> 3) + (pres ? (((uint64_t)n * wr + 7) >> 3) : 0);
+}
+
+template <int D, typename T>
+__global__ void __launch_bounds__(256) k_geometry(const EncParams P) {
+  const uint64_t blk = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  DevResult* R = P.res;
+  double eb_abs = P.eb;
+  if (P.rel) {  // model.py:194-199, identical IEEE ops
+    const double glo = -ukey_inv(R->range_w[0]);
+    const double ghi = ukey_inv(R->range_w[1]);
+    double span = __dsub_rn(ghi, glo);
+    if (span <= 0.0) span = 1.0;
+    eb_abs = __dmul_rn(P.eb, span);
+  }
+  if (blk == 0) R->eb_abs = eb_abs;
+  if (blk >= P.nblocks) return;
+  const T* bnd = reinterpret_cast<const T*>(P.bounds) + blk * 2 * D;
+  BlkRec rec;
+  memset(&rec, 0, sizeof(rec));
+  int err = R_NONE, eax = 0;
+  AxisGeo g[D];
+  if (!(eb_abs > 0.0)) {
+    err = R_EB_NOT_POSITIVE;
+  } else {
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      if (!err && axis_geometry((double)bnd[2 * a], (double)bnd[2 * a + 1], eb_abs, sizeof(T) == 8, P.target, g[a])) {
+        err = R_AXIS_RANGE;
+        eax = a;
+      }
+    }
+  }
+  unsigned __int128 PN = 1;
+  uint32_t sumb = 0;
+  bool narrow = !P.preserve;
+  if (!err) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      PN *= g[a].N;
+      if (PN > ((unsigned __int128)1 << 64)) { err = R_GEOMETRY; break; }
+      sumb += g[a].b;
+      narrow = narrow && g[a].mode == 0;
+      rec.lo[a] = g[a].lo;
+      rec.rinv[a] = g[a].rinv;
+      rec.w[a] = g[a].w;
+      rec.N[a] = (uint32_t)g[a].N;
+      rec.b[a] = (uint8_t)g[a].b;
+    }
+    if (!err && sumb > 64) err = R_GEOMETRY;
+  }
+  if (err) {
+    rec.kind = KIND_ERROR;
+    atomicMax(&R->err_block, err_code(blk, eax, err));
+  } else {
+    narrow = narrow && PN <= 65536 && sumb <= 32;
+    rec.PN = narrow ? (uint32_t)PN : 0u;
+    rec.sumb = (uint8_t)sumb;
+    if (narrow) {
+      rec.kind = KIND_NARROW;
+    } else {
+      rec.kind = KIND_WIDE;
+      const uint32_t n = (uint32_t)min((uint64_t)P.bs, P.count - blk * (uint64_t)P.bs);
+      const uint32_t wdel = (uint32_t)bitlen64((uint64_t)(PN - 1));
+      const uint64_t lb = (payload_bound(D, sizeof(T), P.preserve, n, wdel, sumb) + 15) & ~15ull;
+      rec.side_off = atomicAdd(&R->side_bytes, (unsigned long long)lb);
+      const uint32_t slot = atomicAdd(&R->wide_count, 1u);
+      P.wide_list[slot] = (uint32_t)blk;
+    }
+  }
+  reinterpret_cast<BlkRec*>(P.rec)[blk] = rec;
+}
+
+// --------------------------------------------------- shared K2 building blocks
+// Bitmap rank machinery: zero / set / prefix.  Words [0, nw) of bm, prefix
+// counts into wp.  bm_prefix returns the number of set bits.
 __device__ __forceinline__ void bm_zero(uint32_t* bm, int nw) {
   for (int w = threadIdx.x; w < nw; w += kThreads) bm[w] = 0u;
 }
@@ -256,442 +341,59 @@ __device__ __forceinline__ void put_le(uint8_t* dst, uint64_t v, int nbytes) {
   for (int i = 0; i < nbytes; ++i) dst[i] = (uint8_t)(v >> (8 * i));
 }
 
-template <int D, bool F64, bool PRES>
-__global__ void __launch_bounds__(kThreads) k_encode(const EncParams P) {
-  using T = typename std::conditional<F64, double, float>::type;
-  constexpr int S = F64 ? 8 : 4;
-  constexpr int H = 8 + D * (2 * S + 5) + (PRES ? 4 : 3);  // block header bytes (container.py:62-67)
-  constexpr unsigned long long FA = 1ull << 62, FP = 2ull << 62, VM = FA - 1;
-  __shared__ EncSmem sm;
-  const int tid = threadIdx.x, lane = tid & 31;
-  DevResult* R = P.res;
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = kFlagAgg - 1;
 
-  if (tid == 0) sm.blk = atomicAdd(&R->ticket, 1ull);
-  __syncthreads();
-  const uint64_t blk = sm.blk;
-  const uint64_t first = blk * (uint64_t)P.bs;
-  const int n = (int)min((uint64_t)P.bs, P.count - first);
-  const int p0 = tid * kItems;
-
-  // ---- 1. load the block (coalesced 16B loads, evict-first)
-  T x[D][kItems];
-  load_particles<D, T>(P, first, n, p0, x);
-
-  // ---- 2. block bounds: from K1 (REL) or reduced here (ABS)
-  double lo[D], hi[D];
-  if (P.rel) {
-    const T* b = reinterpret_cast<const T*>(P.bounds) + blk * 2 * D;
-#pragma unroll
-    for (int a = 0; a < D; ++a) { lo[a] = (double)b[2 * a]; hi[a] = (double)b[2 * a + 1]; }
-  } else {
-    uint32_t nf;
-    block_bounds<D, T>(x, n, p0, lo, hi, nf, sm.redd);
-    if (lane == 0 && nf) atomicOr(&R->nonfinite_mask, nf);
-  }
-  double eb_abs = P.eb;
-  if (P.rel) {  // model.py:194-199, identical IEEE ops
-    double glo = -ukey_inv(R->range_w[0]);
-    double ghi = ukey_inv(R->range_w[1]);
-    double span = __dsub_rn(ghi, glo);
-    if (span <= 0.0) span = 1.0;
-    eb_abs = __dmul_rn(P.eb, span);
-  }
-
-  // ---- 3. geometry (one thread per axis)
-  if (tid < D) sm.ax_err[tid] = axis_geometry(lo[tid], hi[tid], eb_abs, F64, P.target, sm.geo[tid]);
-  __syncthreads();
-  int err = R_NONE, err_axis = 0;
-  if (!(eb_abs > 0.0)) {
-    err = R_EB_NOT_POSITIVE;
-  } else {
-#pragma unroll
-    for (int a = D - 1; a >= 0; --a)
-      if (sm.ax_err[a]) { err = R_AXIS_RANGE; err_axis = a; }
-  }
-  unsigned __int128 PN = 1;
-  uint32_t sumb = 0;
-  uint64_t stride[D];
-  uint32_t shift[D];
-  if (!err) {
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      stride[a] = (uint64_t)PN;  // Π N of earlier axes (<= 2^64 checked below)
-      shift[a] = sumb;
-      PN *= sm.geo[a].N;
-      if (PN > ((unsigned __int128)1 << 64)) { err = R_GEOMETRY; break; }
-      sumb += sm.geo[a].b;
+// Decoupled look-back (one warp): exclusive prefix of block `blk` from the
+// predecessors' aggregate / inclusive words.
+__device__ __forceinline__ uint64_t lookback_warp(unsigned long long* status, uint64_t blk) {
+  const int lane = threadIdx.x & 31;
+  uint64_t excl = 0;
+  long long look = (long long)blk - 1;
+  while (look >= 0) {
+    const long long idx = look - lane;
+    unsigned long long v = kFlagInc;
+    if (idx >= 0) {
+      do { v = ld_acquire(&status[idx]); } while ((v >> 62) == 0);
     }
-    if (sumb > 64) err = R_GEOMETRY;
+    const unsigned pm = __ballot_sync(kFull, (v >> 62) == 2);
+    const int lim = pm ? __ffs(pm) - 1 : 31;
+    unsigned long long c = (lane <= lim) ? (v & kValMask) : 0ull;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+    excl += c;
+    if (pm) break;
+    look -= 32;
   }
+  return excl;
+}
 
-  // ---- 4. quantize + linearize (quantizer.py:142-191)
-  uint64_t seg[kItems], off[kItems];
-  uint64_t off_or = 0;
-  if (!err) {
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) { seg[k] = 0; off[k] = 0; }
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      const AxisGeo g = sm.geo[a];
-      const uint64_t mk = mask64(g.b);
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        if (p0 + k < n) {
-          uint64_t q = quantize_coord((double)x[a][k], g, eb_abs, F64);
-          seg[k] += shr64(q, g.b) * stride[a];
-          off[k] |= shl64(q & mk, shift[a]);
-        }
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) off_or |= (p0 + k < n) ? off[k] : 0ull;
-  }
-
-  // ---- 5. counting sort + run-length statistics
-  const bool passA = !err && PN <= 65536;
-  uint32_t srank[kItems], tie[kItems], pos[kItems];
-  uint32_t rk[kItems];  // original intra-block index (rank stream)
-  uint32_t U = 0;
-  int path = 0;
-#pragma unroll
-  for (int k = 0; k < kItems; ++k) { srank[k] = tie[k] = 0; pos[k] = p0 + k; rk[k] = p0 + k; }
-
-  if (passA) {
-    // distinct-segment ranks from a presence bitmap over [0, ΠN)
-    const int nw = (int)(((uint32_t)PN + 31) >> 5);
-    bm_zero(sm.u.a.bm, nw);
-    reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kItems; ++k)
-      if (p0 + k < n) atomicOr(&sm.u.a.bm[seg[k] >> 5], 1u << (seg[k] & 31));
-    __syncthreads();
-    U = bm_prefix(sm.u.a.bm, sm.u.a.wp, nw, sm.scan32);
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kItems; ++k)
-      if (p0 + k < n) {
-        srank[k] = bm_rank(sm.u.a.bm, sm.u.a.wp, (uint32_t)seg[k]);
-        tie[k] = atomicAdd(&sm.cnt[srank[k]], 1u);
-        sm.uniq[srank[k]] = seg[k];
-      }
-    __syncthreads();
-  } else if (!err) {
-    // general key width: stable LSD over (segment, offset) with 5-bit digits
-    path = 4;
-    const uint32_t segbits = (uint32_t)bitlen64((uint64_t)(PN - 1));
-    const uint32_t total_bits = sumb + segbits;
-    for (uint32_t s = 0; s < total_bits; s += 5) {
-      const int dlen = (int)min(5u, total_bits - s);
-      uint32_t dig[kItems], np[kItems];
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        uint64_t v = s < sumb ? shr64(off[k], s) : shr64(seg[k], s - sumb);
-        if (s < sumb && s + dlen > sumb) v = (off[k] >> s) | shl64(seg[k], sumb - s);
-        dig[k] = (uint32_t)(v & ((1u << dlen) - 1u));
-      }
-      lsd_ranks(dig, dlen, n, p0, sm.u.g.bm, sm.u.g.wp, sm.scan32, np);
-#pragma unroll
-      for (int k = 0; k < kItems; ++k)
-        if (p0 + k < n) { sm.u.g.off[np[k]] = off[k]; sm.u.g.seg[np[k]] = seg[k]; sm.u.g.rk[np[k]] = (uint16_t)rk[k]; }
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < kItems; ++k)
-        if (p0 + k < n) { off[k] = sm.u.g.off[p0 + k]; seg[k] = sm.u.g.seg[p0 + k]; rk[k] = sm.u.g.rk[p0 + k]; }
-      __syncthreads();
-    }
-    // run-length factorisation of the sorted segment ids (codec.py:53-79)
-    sm.u.g.seg[p0 + 3 < kMaxBs ? p0 + 3 : kMaxBs - 1] = sm.u.g.seg[p0 + 3 < kMaxBs ? p0 + 3 : kMaxBs - 1];
-    uint32_t flag[kItems], nflag = 0;
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      const int p = p0 + k;
-      uint64_t prev = (k > 0) ? seg[k - 1] : (p > 0 ? sm.u.g.seg[p - 1] : 0);
-      flag[k] = (p < n) && (p == 0 || seg[k] != prev);
-      nflag += flag[k];
-    }
-    uint32_t tot;
-    uint32_t run = block_excl_scan<uint32_t>(nflag, tot, sm.scan32);
-    U = tot;
-#pragma unroll
-    for (int k = 0; k < kItems; ++k)
-      if (flag[k]) { sm.uniq[run] = seg[k]; sm.cnt[run] = (uint32_t)(p0 + k); ++run; }
-    __syncthreads();
-    uint32_t cs[kItems];
-#pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-      const uint32_t r = p0 + j;
-      cs[j] = (r < U) ? ((r + 1 < U ? sm.cnt[r + 1] : (uint32_t)n) - sm.cnt[r]) : 0u;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kItems; ++j)
-      if (p0 + j < (int)U) sm.cnt[p0 + j] = cs[j];
-    __syncthreads();
-  }
-
-  // ---- 6. stream widths (codec.width_for == bit length of the OR) and size
-  uint32_t cnt_or = 0, cmax_dummy = 0;
-  uint64_t del_or = 0;
-  uint32_t cloc[kItems], csum = 0;
-  (void)cmax_dummy;
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const uint32_t r = p0 + j;
-    cloc[j] = 0;
-    if (!err && r < U) {
-      cloc[j] = sm.cnt[r];
-      cnt_or |= cloc[j];
-      del_or |= sm.uniq[r] - (r ? sm.uniq[r - 1] : 0ull);
-      csum += cloc[j];
-    }
-  }
-  uint32_t red[5] = {(uint32_t)off_or, (uint32_t)(off_or >> 32), cnt_or, (uint32_t)del_or,
-                     (uint32_t)(del_or >> 32)};
-  block_or<5>(red, sm.red);
-  const uint32_t w_off = bitlen64((uint64_t)red[0] | ((uint64_t)red[1] << 32));
-  const uint32_t w_cnt = bitlen32(red[2]);
-  const uint32_t w_del = bitlen64((uint64_t)red[3] | ((uint64_t)red[4] << 32));
-  const uint32_t w_rank = PRES ? (uint32_t)bitlen32((uint32_t)(n - 1)) : 0u;
-  const uint64_t Ld = ((uint64_t)U * w_del + 7) >> 3;
-  const uint64_t Lc = ((uint64_t)U * w_cnt + 7) >> 3;
-  const uint64_t Lo = ((uint64_t)n * w_off + 7) >> 3;
-  const uint64_t Lr = PRES ? (((uint64_t)n * w_rank + 7) >> 3) : 0;
-  const uint64_t L = err ? 0 : (uint64_t)H + Ld + Lc + Lo + Lr;
-
-  // publish this block's aggregate as early as possible
-  if (tid == 0) st_release(&P.status[blk], (blk == 0 ? FP : FA) | L);
-
-  // ---- 7. order the offset (and rank) stream
-  if (passA) {
-    const bool need = PRES || w_off != 0;
-    if (!need) {
-      path = 0;
-    } else if (!PRES && ((uint64_t)U << sumb) <= 65536) {
-      // pass B: ranks of (segment rank, offset) composites
-      path = 1;
-      const uint32_t range = U << sumb;
-      const int nw = (int)((range + 31) >> 5);
-      bm_zero(sm.u.b.bm, nw);
-      reinterpret_cast<uint4*>(sm.u.b.cnt2)[tid] = make_uint4(0, 0, 0, 0);
-      __syncthreads();
-      uint32_t c[kItems];
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        c[k] = (srank[k] << sumb) | (uint32_t)off[k];
-        if (p0 + k < n) atomicOr(&sm.u.b.bm[c[k] >> 5], 1u << (c[k] & 31));
-      }
-      __syncthreads();
-      const uint32_t nd = bm_prefix(sm.u.b.bm, sm.u.b.wp, nw, sm.scan32);
-      __syncthreads();
-      uint32_t cr[kItems], t2[kItems];
-#pragma unroll
-      for (int k = 0; k < kItems; ++k)
-        if (p0 + k < n) {
-          cr[k] = bm_rank(sm.u.b.bm, sm.u.b.wp, c[k]);
-          t2[k] = atomicAdd(&sm.u.b.cnt2[cr[k]], 1u);
-        }
-      __syncthreads();
-      uint32_t v[kItems], loc = 0;
-#pragma unroll
-      for (int j = 0; j < kItems; ++j) {
-        v[j] = (p0 + j < (int)nd) ? sm.u.b.cnt2[p0 + j] : 0u;
-        loc += v[j];
-      }
-      uint32_t tot;
-      uint32_t ex = block_excl_scan<uint32_t>(loc, tot, sm.scan32);
-#pragma unroll
-      for (int j = 0; j < kItems; ++j) {
-        if (p0 + j < (int)nd) sm.u.b.cnt2[p0 + j] = ex;
-        ex += v[j];
-      }
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < kItems; ++k)
-        if (p0 + k < n) pos[k] = sm.u.b.cnt2[cr[k]] + t2[k];
-      __syncthreads();
-    } else if (!PRES && w_cnt <= 6) {
-      // small groups: rank by comparison inside each segment's group
-      path = 2;
-      uint32_t tot;
-      uint32_t ex = block_excl_scan<uint32_t>(csum, tot, sm.scan32);
-#pragma unroll
-      for (int j = 0; j < kItems; ++j) {
-        if (p0 + j < (int)U) sm.u.c.segstart[p0 + j] = (uint16_t)ex;
-        ex += cloc[j];
-      }
-      __syncthreads();
-      uint32_t g0[kItems];
-#pragma unroll
-      for (int k = 0; k < kItems; ++k)
-        if (p0 + k < n) {
-          g0[k] = sm.u.c.segstart[srank[k]];
-          sm.u.c.tmp[g0[k] + tie[k]] = off[k];
-        }
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < kItems; ++k)
-        if (p0 + k < n) {
-          const uint32_t gs = sm.cnt[srank[k]], me = g0[k] + tie[k];
-          uint32_t r = 0;
-          for (uint32_t j = g0[k]; j < g0[k] + gs; ++j) {
-            const uint64_t o = sm.u.c.tmp[j];
-            r += (o < off[k]) || (o == off[k] && j < me);
-          }
-          pos[k] = g0[k] + r;
-        }
-      __syncthreads();
-    } else {
-      // stable LSD over (segment rank, offset) with 6-bit digits
-      path = 3;
-      const uint32_t srbits = (uint32_t)bitlen32(U - 1);
-      const uint32_t total_bits = sumb + srbits;
-      for (uint32_t s = 0; s < total_bits; s += 6) {
-        const int dlen = (int)min(6u, total_bits - s);
-        uint32_t dig[kItems], np[kItems];
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) {
-          uint64_t v = s < sumb ? shr64(off[k], s) : (uint64_t)(srank[k] >> (s - sumb));
-          if (s < sumb && s + dlen > sumb) v |= (uint64_t)srank[k] << (sumb - s);
-          dig[k] = (uint32_t)(v & ((1u << dlen) - 1u));
-        }
-        lsd_ranks(dig, dlen, n, p0, sm.u.l.bm, sm.u.l.wp, sm.scan32, np);
-#pragma unroll
-        for (int k = 0; k < kItems; ++k)
-          if (p0 + k < n) {
-            sm.u.l.off[np[k]] = off[k];
-            sm.u.l.sr[np[k]] = (uint16_t)srank[k];
-            sm.u.l.rk[np[k]] = (uint16_t)rk[k];
-          }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kItems; ++k)
-          if (p0 + k < n) {
-            off[k] = sm.u.l.off[p0 + k];
-            srank[k] = sm.u.l.sr[p0 + k];
-            rk[k] = sm.u.l.rk[p0 + k];
-          }
-        __syncthreads();
-      }
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) pos[k] = p0 + k;
-    }
-  }
-
-  // ---- 8. decoupled look-back for this block's payload offset
-  if (tid < 32) {
-    uint64_t excl = 0;
-    long long look = (long long)blk - 1;
-    while (look >= 0) {
-      const long long idx = look - lane;
-      unsigned long long v = FP;
-      if (idx >= 0) {
-        do { v = ld_acquire(&P.status[idx]); } while ((v >> 62) == 0);
-      }
-      const unsigned pm = __ballot_sync(kFull, (v >> 62) == 2);
-      const int lim = pm ? __ffs(pm) - 1 : 31;
-      unsigned long long c = (lane <= lim) ? (v & VM) : 0ull;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-      excl += c;
-      if (pm) break;
-      look -= 32;
-    }
-    if (lane == 0) {
-      sm.excl = excl;
-      if (blk > 0) st_release(&P.status[blk], FP | (excl + L));
-      if (blk + 1 == P.nblocks) R->total_payload = excl + L;
-      if (err) atomicMax(&R->err_block, err_code(blk, err_axis, err));
-      atomicAdd(&R->path_blocks[err ? 5 : path], 1ull);
-    }
-    if (lane < 8) P.table[blk * 8 + lane] = (uint8_t)((P.table_base + excl + L) >> (8 * lane));
-  }
-  __syncthreads();
-  const uint64_t excl = sm.excl;
-
-  // ---- global header + table entry 0 (block 0 only; container.py:211-230)
-  if (blk == 0 && tid == 32) {
-    if (P.table0) put_le(P.table0, P.table_base, 8);
-    if (P.header) {
-      uint8_t* h = P.header;
-      h[0] = 'G'; h[1] = 'P'; h[2] = 'Z'; h[3] = '1';
-      put_le(h + 4, 1, 2);
-      h[6] = (uint8_t)D;
-      h[7] = F64 ? 1 : 0;
-      h[8] = PRES ? 1 : 0;
-      h[9] = (uint8_t)P.eb_mode_code;
-      put_le(h + 10, (uint64_t)__double_as_longlong(P.eb), 8);
-      put_le(h + 18, (uint64_t)__double_as_longlong(eb_abs), 8);
-      put_le(h + 26, P.bs, 4);
-      put_le(h + 30, P.header_count, 8);
-      put_le(h + 38, P.header_blocks, 8);
-      R->eb_abs = eb_abs;
-    }
-  }
-  if (err) return;
-
-  // ---- 9. bit-pack header + streams into the realigned stage
-  uint8_t* dst = P.payload + excl;
+// Copy `len` payload bytes held at byte 0.. of the u32 word array `src`
+// (shared or global, 16B aligned) to an arbitrary global address, as
+// 16-byte vector stores for the chunks the block owns outright and byte
+// stores for the two edge chunks shared with the neighbouring payloads.
+template <typename Src>
+__device__ __forceinline__ void realign_copy(uint8_t* dst, const Src* src, uint32_t len, int tid, int nthreads) {
   const uint32_t al = (uint32_t)((uintptr_t)dst & 15);
-  const uint32_t nbytes = al + (uint32_t)L;
-  const uint32_t nch = (nbytes + 15) >> 4;
-  uint32_t* st = sm.u.stage;
-  for (uint32_t c = tid; c < nch; c += kThreads) reinterpret_cast<uint4*>(st)[c] = make_uint4(0, 0, 0, 0);
-  __syncthreads();
-  const uint64_t base = 8ull * al;
-  if (tid < 32) {
-    // header fields, one per lane (container.serialize_block, container.py:107-121)
-    int f = lane;
-    uint64_t bpos = 0, val = 0;
-    bool act = true;
-    if (f == 0) { bpos = 0; val = (uint32_t)n; }
-    else if (f == 1) { bpos = 4; val = U; }
-    else if (f < 2 + 4 * D) {
-      const int a = (f - 2) >> 2, which = (f - 2) & 3;
-      const uint64_t ab = 8 + (uint64_t)a * (2 * S + 5);
-      const AxisGeo& g = sm.geo[a];
-      if (which == 0) { bpos = ab; val = F64 ? (uint64_t)__double_as_longlong(g.lo) : (uint64_t)__float_as_uint((float)g.lo); }
-      else if (which == 1) { bpos = ab + S; val = F64 ? (uint64_t)__double_as_longlong(g.hi) : (uint64_t)__float_as_uint((float)g.hi); }
-      else if (which == 2) { bpos = ab + 2 * S; val = g.b; }
-      else { bpos = ab + 2 * S + 1; val = (uint32_t)g.N; }
-    } else if (f < 2 + 4 * D + (PRES ? 4 : 3)) {
-      const int wi = f - 2 - 4 * D;
-      bpos = 8 + (uint64_t)D * (2 * S + 5) + wi;
-      val = wi == 0 ? w_del : wi == 1 ? w_cnt : wi == 2 ? w_off : w_rank;
-    } else {
-      act = false;
-    }
-    if (act) or_bits(st, base + 8 * bpos, val);
-  }
-  const uint64_t bd = base + 8ull * H;
-  const uint64_t bc = bd + 8ull * Ld;
-  const uint64_t bo = bc + 8ull * Lc;
-  const uint64_t br = bo + 8ull * Lo;
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const uint32_t r = p0 + j;
-    if (r < U) {
-      if (w_del) or_bits(st, bd + (uint64_t)r * w_del, sm.uniq[r] - (r ? sm.uniq[r - 1] : 0ull));
-      if (w_cnt) or_bits(st, bc + (uint64_t)r * w_cnt, cloc[j]);
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < kItems; ++k)
-    if (p0 + k < n) {
-      if (w_off) or_bits(st, bo + (uint64_t)pos[k] * w_off, off[k]);
-      if (PRES && w_rank) or_bits(st, br + (uint64_t)pos[k] * w_rank, rk[k]);
-    }
-  __syncthreads();
-
-  // ---- 10. write out: full 16B chunks as vector stores, shared edges bytewise
   uint8_t* g16 = dst - al;
-  for (uint32_t c = tid; c < nch; c += kThreads) {
-    const uint4 v = reinterpret_cast<const uint4*>(st)[c];
+  const uint32_t nbytes = al + len;
+  const uint32_t nch = (nbytes + 15) >> 4;
+  const uint32_t nwords = (len + 3) >> 2;
+  const uint32_t sh = ((4 - (al & 3)) & 3) * 8;  // byte shift between source and destination words
+  for (uint32_t c = tid; c < nch; c += nthreads) {
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      // destination bytes [16c + 4j, +4) hold payload bytes starting at s
+      const int s = (int)(16 * c + 4 * j) - (int)al;
+      const int wi = s >> 2;  // floor (s may be negative)
+      const uint32_t lo = (wi >= 0 && (uint32_t)wi < nwords) ? (uint32_t)src[wi] : 0u;
+      const uint32_t hi = (wi + 1 >= 0 && (uint32_t)(wi + 1) < nwords) ? (uint32_t)src[wi + 1] : 0u;
+      w[j] = sh ? __funnelshift_r(lo, hi, sh) : lo;
+    }
     const uint32_t b0 = c * 16;
     if (b0 >= al && b0 + 16 <= nbytes) {
-      __stcs(reinterpret_cast<uint4*>(g16 + b0), v);
+      __stcs(reinterpret_cast<uint4*>(g16 + b0), make_uint4(w[0], w[1], w[2], w[3]));
     } else {
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int j = 0; j < 16; ++j)
         if (b0 + j >= al && b0 + j < nbytes) g16[b0 + j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));

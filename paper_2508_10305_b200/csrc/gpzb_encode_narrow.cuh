@@ -1,0 +1,381 @@
+// K2: the 32-bit fast block encoder + container assembly.
+//
+// One CTA (256 threads x 4 particles) per block, blocks taken in ticket
+// order for the decoupled look-back.  For "narrow" blocks (K1.5: every axis
+// on the certified-reciprocal quantizer, Π N <= 2^16, Σ log2 m <= 32, no
+// rank stream) it does the whole of pipeline._encode_block (pipeline.py:38-70):
+//
+//   quantize (quantizer.py:142-191)  -> 32-bit (segment, offset) per particle
+//   pass A: presence bitmap over [0, Π N) -> distinct-segment ranks, run
+//           lengths and unique ids in one pass (RLE, codec.py:53-79)
+//   pass B: presence bitmap over (segment rank, offset) -> the stable
+//           (seg, off) order of blocksort.py:17-28 (ties are identical pairs)
+//   widths (codec.width_for) by OR-reduction, payload size, aggregate publish
+//   warp 0: decoupled look-back | warps 1-7: bit-pack header + streams
+//   all: realigned 16-byte vector stores of the payload + the table entry.
+//
+// Wide and error blocks only take part in the look-back and copy the
+// payload staged by K2w.
+#pragma once
+
+#include "gpzb_encode.cuh"
+
+namespace gpzb {
+
+#ifndef GPZB_K2_MINB
+#define GPZB_K2_MINB 4
+#endif
+constexpr int kNarrowStageWords = 2048 + 32;  // narrow payload <= 7.7 KB
+
+struct NarrowSmem {
+  uint64_t blk;
+  uint64_t excl;
+  uint32_t red[kWarps * 4];
+  uint32_t scan32[kWarps];
+  __align__(16) uint32_t cnt[kMaxBs];   // run length per distinct segment rank
+  __align__(16) uint32_t soff[kMaxBs];  // offsets in sorted order
+  __align__(16) uint16_t uniq[kMaxBs];  // unique segment ids (Π N <= 2^16)
+  union U {
+    struct { uint32_t bm[2048]; uint16_t wp[2048]; } a;
+    struct { uint32_t bm[2048]; uint16_t wp[2048]; uint32_t cnt2[kMaxBs]; } b;
+    struct { uint16_t segstart[kMaxBs]; uint32_t tmp[kMaxBs]; } c;
+    struct { uint32_t off[kMaxBs]; uint16_t sr[kMaxBs]; uint32_t bm[1024]; uint16_t wp[1024]; } l;
+    uint32_t stage[kNarrowStageWords];
+  };
+  __align__(16) U u;
+};
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Global header (container.py:211-230) and table entry 0, by one thread of block 0.
+template <int D, bool F64>
+__device__ void write_global_header(const EncParams& P, double eb_abs) {
+  if (P.table0) put_le(P.table0, P.table_base, 8);
+  if (!P.header) return;
+  uint8_t* h = P.header;
+  h[0] = 'G'; h[1] = 'P'; h[2] = 'Z'; h[3] = '1';
+  put_le(h + 4, 1, 2);
+  h[6] = (uint8_t)D;
+  h[7] = F64 ? 1 : 0;
+  h[8] = P.preserve ? 1 : 0;
+  h[9] = (uint8_t)P.eb_mode_code;
+  put_le(h + 10, (uint64_t)__double_as_longlong(P.eb), 8);
+  put_le(h + 18, (uint64_t)__double_as_longlong(eb_abs), 8);
+  put_le(h + 26, P.bs, 4);
+  put_le(h + 30, P.header_count, 8);
+  put_le(h + 38, P.header_blocks, 8);
+}
+
+// Look-back by warp 0 for a block of payload length L (aggregate already
+// published); writes its table entry and publishes the inclusive prefix.
+__device__ __forceinline__ uint64_t finish_lookback(const EncParams& P, uint64_t blk, uint64_t L) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t excl = blk ? lookback_warp(P.status, blk) : 0ull;
+  if (lane == 0) {
+    if (blk > 0) st_release(&P.status[blk], kFlagInc | (excl + L));
+    if (blk + 1 == P.nblocks) P.res->total_payload = excl + L;
+  }
+  if (lane < 8) P.table[blk * 8 + lane] = (uint8_t)((P.table_base + excl + L) >> (8 * lane));
+  return excl;
+}
+
+template <int D, bool F64>
+__global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncParams P) {
+  using T = typename std::conditional<F64, double, float>::type;
+  constexpr int S = F64 ? 8 : 4;
+  constexpr uint32_t H = 8 + D * (2 * S + 5) + 3;  // block header bytes (container.py:62-67)
+  __shared__ NarrowSmem sm;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  DevResult* R = P.res;
+
+  if (tid == 0) sm.blk = atomicAdd(&R->ticket, 1ull);
+  __syncthreads();
+  const uint64_t blk = sm.blk;
+  const BlkRec* rec = P.rec + blk;
+  const uint32_t kind = rec->kind;
+  if (blk == 0 && tid == 32) write_global_header<D, F64>(P, R->eb_abs);
+
+  if (kind != KIND_NARROW) {
+    // wide (staged by K2w) or error block (size 0): look-back + copy only
+    const uint64_t L = (kind == KIND_WIDE) ? rec->side_len : 0ull;
+    if (tid == 0) st_release(&P.status[blk], (blk == 0 ? kFlagInc : kFlagAgg) | L);
+    if (wid == 0) {
+      const uint64_t ex = finish_lookback(P, blk, L);
+      if (lane == 0) sm.excl = ex;
+    }
+    __syncthreads();
+    if (L) realign_copy(P.payload + sm.excl, reinterpret_cast<const uint32_t*>(P.side + rec->side_off),
+                        (uint32_t)L, tid, kThreads);
+    return;
+  }
+
+  const uint64_t first = blk * (uint64_t)P.bs;
+  const int n = (int)min((uint64_t)P.bs, P.count - first);
+  const int p0 = tid * kItems;
+
+  // ---- 1. load + quantize to 32-bit (segment, offset)
+  T x[D][kItems];
+  load_particles<D, T>(P, first, n, p0, x);
+  const uint32_t PN = rec->PN, sumb = rec->sumb;
+  uint32_t seg[kItems], off[kItems];
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) { seg[k] = 0; off[k] = 0; }
+  {
+    uint32_t stride = 1, shift = 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const double lo = rec->lo[a], rinv = rec->rinv[a], w = rec->w[a];
+      const uint32_t b = rec->b[a];
+      const uint32_t mk = (1u << b) - 1u;
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        // certified reciprocal quantizer (gpzb_common.cuh quantize_coord, mode 0)
+        const double t = __dsub_rn((double)x[a][k], lo);
+        const double r = __dmul_rn(t, rinv);
+        const uint32_t rl = (uint32_t)__double2loint(r), rh = (uint32_t)__double2hiint(r);
+        uint32_t q = (uint32_t)__double2loint(__dadd_rz(r, 4503599627370496.0));
+        if ((rl + 1u) <= 1u && (rl | rh) != 0u) q = __double2uint_rz(__ddiv_rn(t, w));
+        seg[k] += (q >> b) * stride;
+        if (b) off[k] |= (q & mk) << shift;
+      }
+      stride *= rec->N[a];
+      shift += b;
+    }
+  }
+  uint32_t off_or = 0;
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) off_or |= (p0 + k < n) ? off[k] : 0u;
+
+  // ---- 2. pass A: distinct-segment ranks, run lengths, unique ids
+  const int nwA = (int)((PN + 31) >> 5);
+  bm_zero(sm.u.a.bm, nwA);
+  reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kItems; ++k)
+    if (p0 + k < n) atomicOr(&sm.u.a.bm[seg[k] >> 5], 1u << (seg[k] & 31));
+  __syncthreads();
+  const uint32_t U = bm_prefix(sm.u.a.bm, sm.u.a.wp, nwA, sm.scan32);
+  __syncthreads();
+  uint32_t srank[kItems], tie[kItems];
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    srank[k] = tie[k] = 0;
+    if (p0 + k < n) {
+      srank[k] = bm_rank(sm.u.a.bm, sm.u.a.wp, seg[k]);
+      tie[k] = atomicAdd(&sm.cnt[srank[k]], 1u);
+      sm.uniq[srank[k]] = (uint16_t)seg[k];
+    }
+  }
+  __syncthreads();
+
+  // ---- 3. stream widths (width_for == bit length of the OR) and payload size
+  uint32_t cloc[kItems], csum = 0, c_or = 0, d_or = 0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const uint32_t r = p0 + j;
+    cloc[j] = 0;
+    if (r < U) {
+      cloc[j] = sm.cnt[r];
+      c_or |= cloc[j];
+      d_or |= (uint32_t)sm.uniq[r] - (r ? (uint32_t)sm.uniq[r - 1] : 0u);
+      csum += cloc[j];
+    }
+  }
+  uint32_t red[3] = {off_or, c_or, d_or};
+  block_or<3>(red, sm.red);
+  const uint32_t w_off = bitlen32(red[0]), w_cnt = bitlen32(red[1]), w_del = bitlen32(red[2]);
+  const uint32_t Ld = (U * w_del + 7) >> 3, Lc = (U * w_cnt + 7) >> 3, Lo = ((uint32_t)n * w_off + 7) >> 3;
+  const uint32_t L = H + Ld + Lc + Lo;
+  if (tid == 0) st_release(&P.status[blk], (blk == 0 ? kFlagInc : kFlagAgg) | L);
+
+  // ---- 4. order the offsets: (segment rank, offset) composite ranks
+  int path = 0;
+  if (w_off) {
+    uint32_t pos[kItems];
+    if (sumb <= 16 && (U << sumb) <= 65536u) {
+      path = 1;
+      const int nw = (int)(((U << sumb) + 31) >> 5);
+      bm_zero(sm.u.b.bm, nw);
+      reinterpret_cast<uint4*>(sm.u.b.cnt2)[tid] = make_uint4(0, 0, 0, 0);
+      __syncthreads();
+      uint32_t c[kItems];
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        c[k] = (srank[k] << sumb) | off[k];
+        if (p0 + k < n) atomicOr(&sm.u.b.bm[c[k] >> 5], 1u << (c[k] & 31));
+      }
+      __syncthreads();
+      const uint32_t nd = bm_prefix(sm.u.b.bm, sm.u.b.wp, nw, sm.scan32);
+      __syncthreads();
+      uint32_t cr[kItems], t2[kItems];
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        cr[k] = t2[k] = 0;
+        if (p0 + k < n) {
+          cr[k] = bm_rank(sm.u.b.bm, sm.u.b.wp, c[k]);
+          t2[k] = atomicAdd(&sm.u.b.cnt2[cr[k]], 1u);
+        }
+      }
+      __syncthreads();
+      uint32_t v[kItems], loc = 0;
+#pragma unroll
+      for (int j = 0; j < kItems; ++j) {
+        v[j] = (p0 + j < (int)nd) ? sm.u.b.cnt2[p0 + j] : 0u;
+        loc += v[j];
+      }
+      uint32_t tot;
+      uint32_t ex = block_excl_scan<uint32_t>(loc, tot, sm.scan32);
+#pragma unroll
+      for (int j = 0; j < kItems; ++j) {
+        if (p0 + j < (int)nd) sm.u.b.cnt2[p0 + j] = ex;
+        ex += v[j];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) pos[k] = (p0 + k < n) ? sm.u.b.cnt2[cr[k]] + t2[k] : 0u;
+    } else if (w_cnt <= 6) {
+      // segment groups of <= 63 particles: rank by comparison inside the group
+      path = 2;
+      uint32_t tot;
+      uint32_t ex = block_excl_scan<uint32_t>(csum, tot, sm.scan32);
+#pragma unroll
+      for (int j = 0; j < kItems; ++j) {
+        if (p0 + j < (int)U) sm.u.c.segstart[p0 + j] = (uint16_t)ex;
+        ex += cloc[j];
+      }
+      __syncthreads();
+      uint32_t g0[kItems];
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        g0[k] = 0;
+        if (p0 + k < n) {
+          g0[k] = sm.u.c.segstart[srank[k]];
+          sm.u.c.tmp[g0[k] + tie[k]] = off[k];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        pos[k] = 0;
+        if (p0 + k < n) {
+          const uint32_t gs = sm.cnt[srank[k]], me = g0[k] + tie[k];
+          uint32_t rr = 0;
+          for (uint32_t j = g0[k]; j < g0[k] + gs; ++j) {
+            const uint32_t o = sm.u.c.tmp[j];
+            rr += (o < off[k]) || (o == off[k] && j < me);
+          }
+          pos[k] = g0[k] + rr;
+        }
+      }
+    } else {
+      // large groups and a wide composite: stable LSD, 5-bit digits
+      path = 3;
+      const uint32_t total_bits = sumb + (uint32_t)bitlen32(U - 1);
+      for (uint32_t s = 0; s < total_bits; s += 5) {
+        const int dlen = (int)min(5u, total_bits - s);
+        uint32_t dig[kItems], np[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const uint64_t key = ((uint64_t)srank[k] << sumb) | off[k];
+          dig[k] = (uint32_t)(key >> s) & ((1u << dlen) - 1u);
+        }
+        lsd_ranks(dig, dlen, n, p0, sm.u.l.bm, sm.u.l.wp, sm.scan32, np);
+#pragma unroll
+        for (int k = 0; k < kItems; ++k)
+          if (p0 + k < n) { sm.u.l.off[np[k]] = off[k]; sm.u.l.sr[np[k]] = (uint16_t)srank[k]; }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kItems; ++k)
+          if (p0 + k < n) { off[k] = sm.u.l.off[p0 + k]; srank[k] = sm.u.l.sr[p0 + k]; }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) pos[k] = p0 + k;
+    }
+#pragma unroll
+    for (int k = 0; k < kItems; ++k)
+      if (p0 + k < n) sm.soff[pos[k]] = off[k];
+  }
+  __syncthreads();  // soff complete; union free for the stage
+
+  // ---- 5. warp 0: look-back | warps 1-7: bit-pack into the stage (payload byte 0 = stage byte 0)
+  uint32_t* st = sm.u.stage;
+  if (wid == 0) {
+    const uint64_t ex = finish_lookback(P, blk, L);
+    if (lane == 0) {
+      sm.excl = ex;
+      atomicAdd(&R->path_blocks[path], 1ull);
+    }
+  } else {
+    const int t = tid - 32, nt = kThreads - 32;
+    const uint32_t nwords = (L + 3) >> 2;
+    for (uint32_t w = t; w < nwords; w += nt) st[w] = 0u;
+    named_sync(1, nt);
+    if (t < 32) {
+      // block header fields, one per lane (container.serialize_block, container.py:107-121)
+      const int f = t;
+      uint32_t bpos = 0;
+      uint64_t val = 0;
+      bool act = true;
+      if (f == 0) { bpos = 0; val = (uint32_t)n; }
+      else if (f == 1) { bpos = 4; val = U; }
+      else if (f < 2 + 4 * D) {
+        const int a = (f - 2) >> 2, which = (f - 2) & 3;
+        const uint32_t ab = 8 + a * (2 * S + 5);
+        const T* bnd = reinterpret_cast<const T*>(P.bounds) + blk * 2 * D;
+        if (which < 2) {
+          bpos = ab + which * S;
+          const T v = bnd[2 * a + which];
+          if constexpr (F64) val = (uint64_t)__double_as_longlong(v);
+          else val = __float_as_uint(v);
+        } else if (which == 2) { bpos = ab + 2 * S; val = rec->b[a]; }
+        else { bpos = ab + 2 * S + 1; val = rec->N[a]; }
+      } else if (f < 2 + 4 * D + 3) {
+        const int wi = f - 2 - 4 * D;
+        bpos = 8 + D * (2 * S + 5) + wi;
+        val = wi == 0 ? w_del : wi == 1 ? w_cnt : w_off;
+      } else {
+        act = false;
+      }
+      if (act) or_bits(st, 8ull * bpos, val);
+    }
+    const uint64_t bd = 8ull * H, bc = bd + 8ull * Ld, bo = bc + 8ull * Lc;
+    // deltas + run lengths, 4 consecutive runs per chunk
+    for (uint32_t r0 = 4 * t; r0 < U; r0 += 4 * nt) {
+      uint64_t dv = 0, cv = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t r = r0 + j;
+        if (r < U) {
+          const uint32_t d = (uint32_t)sm.uniq[r] - (r ? (uint32_t)sm.uniq[r - 1] : 0u);
+          dv |= (uint64_t)d << (j * w_del);
+          cv |= (uint64_t)sm.cnt[r] << (j * w_cnt);
+        }
+      }
+      if (w_del) or_bits(st, bd + (uint64_t)r0 * w_del, dv);
+      if (w_cnt) or_bits(st, bc + (uint64_t)r0 * w_cnt, cv);
+    }
+    // offsets in sorted order, 4 per chunk (two 2-value halves when w_off > 16)
+    if (w_off) {
+      for (uint32_t p = 4 * t; p < (uint32_t)n; p += 4 * nt) {
+        uint64_t v0 = 0, v1 = 0;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (p + j < (uint32_t)n) v0 |= (uint64_t)sm.soff[p + j] << (j * w_off);
+          if (p + 2 + j < (uint32_t)n) v1 |= (uint64_t)sm.soff[p + 2 + j] << (j * w_off);
+        }
+        or_bits(st, bo + (uint64_t)p * w_off, v0);
+        or_bits(st, bo + (uint64_t)(p + 2) * w_off, v1);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- 6. realigned vector stores of the payload
+  realign_copy(P.payload + sm.excl, st, L, tid, kThreads);
+}
+
+}  // namespace gpzb

@@ -144,14 +144,19 @@ def compress_device(ds, cfg: CompressConfig, *, timing=None) -> torch.Tensor:
 
         nb = (count + bs - 1) // bs
         _check(lib.gpzb_workspace_reset_async(ws.data_ptr(), ws.numel(), count, bs, stream))
-        if mode == EbMode.RANGE_RELATIVE.value:
-            e0 = ev() if timing is not None else None
-            _check(lib.gpzb_range_async(ptrs, dims, prec, count, bs, ws.data_ptr(), ws.numel(), stream))
-            if timing is not None:
-                timing.setdefault("range", []).append((e0, ev()))
+        e0 = ev() if timing is not None else None
+        _check(lib.gpzb_range_async(ptrs, dims, prec, count, bs, ws.data_ptr(), ws.numel(), stream))
+        if timing is not None:
+            timing.setdefault("range", []).append((e0, ev()))
+        _check(lib.gpzb_encode_plan_async(ptrs, dims, prec, count, eb, mode, bs, t, pres, ws.data_ptr(),
+                                          ws.numel(), stream))
+        side_bytes = ctypes.c_uint64()
+        _check(lib.gpzb_encode_side_bytes(ws.data_ptr(), ws.numel(), stream, ctypes.byref(side_bytes)))
+        side = torch.empty(max(side_bytes.value, 16), dtype=torch.uint8, device=axes[0].device)
         e0 = ev() if timing is not None else None
         _check(lib.gpzb_encode_async(ptrs, dims, prec, count, eb, mode, bs, t, pres, ws.data_ptr(), ws.numel(),
-                                     out.data_ptr(), bound.value, 0, count, nb, 1, stream))
+                                     side.data_ptr(), side_bytes.value, out.data_ptr(), bound.value, 0, count, nb,
+                                     1, stream))
         if timing is not None:
             timing.setdefault("encode", []).append((e0, ev()))
         st = lib.gpzb_compress_result(ws.data_ptr(), ws.numel(), count, bs, stream, ctypes.byref(res))

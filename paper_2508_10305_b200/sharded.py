@@ -108,12 +108,20 @@ class _CudaHooks:
                                             ctypes.byref(bound)))
         out = torch.empty(bound.value, dtype=torch.uint8, device=self.axes[0].device)
         nb = (ds.count + cfg.block_size - 1) // cfg.block_size
+        args = (self.ptrs, ds.dims, ds.precision.value, ds.count, float(cfg.error_bound), cfg.eb_mode.value,
+                cfg.block_size, cfg.target_segs_per_axis, int(cfg.preserve_order), self.ws.data_ptr(),
+                self.ws.numel())
+        if cfg.eb_mode is not EbMode.RANGE_RELATIVE:  # per-block bounds still come from K1
+            self._check(lib.gpzb_range_async(self.ptrs, ds.dims, ds.precision.value, ds.count, cfg.block_size,
+                                             self.ws.data_ptr(), self.ws.numel(), self._stream()))
+        self._check(lib.gpzb_encode_plan_async(*args, self._stream()))
+        side_bytes = ctypes.c_uint64()
+        self._check(lib.gpzb_encode_side_bytes(self.ws.data_ptr(), self.ws.numel(), self._stream(),
+                                               ctypes.byref(side_bytes)))
+        side = torch.empty(max(side_bytes.value, 16), dtype=torch.uint8, device=self.axes[0].device)
         e0 = self._ev() if self.timing is not None else None
-        self._check(lib.gpzb_encode_async(self.ptrs, ds.dims, ds.precision.value, ds.count,
-                                          float(cfg.error_bound), cfg.eb_mode.value, cfg.block_size,
-                                          cfg.target_segs_per_axis, int(cfg.preserve_order), self.ws.data_ptr(),
-                                          self.ws.numel(), out.data_ptr(), bound.value, 0, ds.count, nb, 1,
-                                          self._stream()))
+        self._check(lib.gpzb_encode_async(*args, side.data_ptr(), side_bytes.value, out.data_ptr(), bound.value,
+                                          0, ds.count, nb, 1, self._stream()))
         if self.timing is not None:
             self.timing.setdefault("encode", []).append((e0, self._ev()))
         res = _lib.Result()
