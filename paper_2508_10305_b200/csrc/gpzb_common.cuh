@@ -102,6 +102,22 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Look-back status words carry their own payload (flag + value in one
+// 64-bit word), so relaxed gpu-scope accesses are sufficient.
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Exact-division fallback of the certified quantizer, kept out of line so
+// the common path is a real branch rather than predicated division code.
+__device__ __noinline__ uint32_t exact_floor_div(double t, double w) {
+  return __double2uint_rz(__ddiv_rn(t, w));
+}
 
 // ------------------------------------------------------- block primitives
 // Exclusive scan over the CTA (one value per thread).  `ws` holds kWarps

@@ -343,26 +343,37 @@ __device__ __forceinline__ void put_le(uint8_t* dst, uint64_t v, int nbytes) {
 
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = kFlagAgg - 1;
 
-// Decoupled look-back (one warp): exclusive prefix of block `blk` from the
-// predecessors' aggregate / inclusive words.
-__device__ __forceinline__ uint64_t lookback_warp(unsigned long long* status, uint64_t blk) {
-  const int lane = threadIdx.x & 31;
+// Decoupled look-back by the whole CTA: each thread inspects one
+// predecessor per round (256 per round), the nearest inclusive prefix ends
+// the walk.  `ws` needs 2*kWarps + 2 words of shared scratch.
+__device__ __forceinline__ uint64_t lookback_cta(unsigned long long* status, uint64_t blk,
+                                                 unsigned long long* ws) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   uint64_t excl = 0;
   long long look = (long long)blk - 1;
   while (look >= 0) {
-    const long long idx = look - lane;
+    const long long idx = look - tid;
     unsigned long long v = kFlagInc;
     if (idx >= 0) {
-      do { v = ld_acquire(&status[idx]); } while ((v >> 62) == 0);
+      do { v = ld_relaxed(&status[idx]); } while ((v >> 62) == 0);
     }
+    // nearest predecessor (smallest tid) holding an inclusive prefix
     const unsigned pm = __ballot_sync(kFull, (v >> 62) == 2);
-    const int lim = pm ? __ffs(pm) - 1 : 31;
-    unsigned long long c = (lane <= lim) ? (v & kValMask) : 0ull;
+    if (lane == 0) ws[wid] = pm ? (unsigned long long)(wid * 32 + __ffs(pm) - 1) : ~0ull;
+    __syncthreads();
+    unsigned long long lim = ~0ull;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) lim = min(lim, ws[w]);
+    unsigned long long c = ((unsigned long long)tid <= lim) ? (v & kValMask) : 0ull;
 #pragma unroll
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-    excl += c;
-    if (pm) break;
-    look -= 32;
+    if (lane == 0) ws[kWarps + wid] = c;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) excl += ws[kWarps + w];
+    __syncthreads();
+    if (lim != ~0ull) break;
+    look -= kThreads;
   }
   return excl;
 }
@@ -395,8 +406,15 @@ __device__ __forceinline__ void realign_copy(uint8_t* dst, const Src* src, uint3
       __stcs(reinterpret_cast<uint4*>(g16 + b0), make_uint4(w[0], w[1], w[2], w[3]));
     } else {
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (b0 + j >= al && b0 + j < nbytes) g16[b0 + j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t wb = b0 + 4 * j;
+        if (wb >= al && wb + 4 <= nbytes) {
+          *reinterpret_cast<uint32_t*>(g16 + wb) = w[j];
+        } else if (wb + 4 > al && wb < nbytes) {
+          for (int q = 0; q < 4; ++q)
+            if (wb + q >= al && wb + q < nbytes) g16[wb + q] = (uint8_t)(w[j] >> (8 * q));
+        }
+      }
     }
   }
 }

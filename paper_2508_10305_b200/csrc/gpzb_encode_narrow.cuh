@@ -30,6 +30,7 @@ constexpr int kNarrowStageWords = 2048 + 32;  // narrow payload <= 7.7 KB
 struct NarrowSmem {
   uint64_t blk;
   uint64_t excl;
+  unsigned long long lb[2 * kWarps + 2];
   uint32_t red[kWarps * 4];
   uint32_t scan32[kWarps];
   __align__(16) uint32_t cnt[kMaxBs];   // run length per distinct segment rank
@@ -68,16 +69,17 @@ __device__ void write_global_header(const EncParams& P, double eb_abs) {
   put_le(h + 38, P.header_blocks, 8);
 }
 
-// Look-back by warp 0 for a block of payload length L (aggregate already
-// published); writes its table entry and publishes the inclusive prefix.
-__device__ __forceinline__ uint64_t finish_lookback(const EncParams& P, uint64_t blk, uint64_t L) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t excl = blk ? lookback_warp(P.status, blk) : 0ull;
-  if (lane == 0) {
-    if (blk > 0) st_release(&P.status[blk], kFlagInc | (excl + L));
+// Look-back by the whole CTA for a block of payload length L (aggregate
+// already published); publishes the inclusive prefix and the table entry.
+__device__ __forceinline__ uint64_t finish_lookback(const EncParams& P, uint64_t blk, uint64_t L,
+                                                    unsigned long long* ws) {
+  const uint64_t excl = blk ? lookback_cta(P.status, blk, ws) : 0ull;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    if (blk > 0) st_relaxed(&P.status[blk], kFlagInc | (excl + L));
     if (blk + 1 == P.nblocks) P.res->total_payload = excl + L;
   }
-  if (lane < 8) P.table[blk * 8 + lane] = (uint8_t)((P.table_base + excl + L) >> (8 * lane));
+  if (tid < 8) P.table[blk * 8 + tid] = (uint8_t)((P.table_base + excl + L) >> (8 * tid));
   return excl;
 }
 
@@ -87,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncPara
   constexpr int S = F64 ? 8 : 4;
   constexpr uint32_t H = 8 + D * (2 * S + 5) + 3;  // block header bytes (container.py:62-67)
   __shared__ NarrowSmem sm;
-  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x;
   DevResult* R = P.res;
 
   if (tid == 0) sm.blk = atomicAdd(&R->ticket, 1ull);
@@ -100,13 +102,9 @@ __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncPara
   if (kind != KIND_NARROW) {
     // wide (staged by K2w) or error block (size 0): look-back + copy only
     const uint64_t L = (kind == KIND_WIDE) ? rec->side_len : 0ull;
-    if (tid == 0) st_release(&P.status[blk], (blk == 0 ? kFlagInc : kFlagAgg) | L);
-    if (wid == 0) {
-      const uint64_t ex = finish_lookback(P, blk, L);
-      if (lane == 0) sm.excl = ex;
-    }
-    __syncthreads();
-    if (L) realign_copy(P.payload + sm.excl, reinterpret_cast<const uint32_t*>(P.side + rec->side_off),
+    if (tid == 0) st_relaxed(&P.status[blk], (blk == 0 ? kFlagInc : kFlagAgg) | L);
+    const uint64_t ex = finish_lookback(P, blk, L, sm.lb);
+    if (L) realign_copy(P.payload + ex, reinterpret_cast<const uint32_t*>(P.side + rec->side_off),
                         (uint32_t)L, tid, kThreads);
     return;
   }
@@ -136,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncPara
         const double r = __dmul_rn(t, rinv);
         const uint32_t rl = (uint32_t)__double2loint(r), rh = (uint32_t)__double2hiint(r);
         uint32_t q = (uint32_t)__double2loint(__dadd_rz(r, 4503599627370496.0));
-        if ((rl + 1u) <= 1u && (rl | rh) != 0u) q = __double2uint_rz(__ddiv_rn(t, w));
+        if ((rl + 1u) <= 1u && (rl | rh) != 0u) q = exact_floor_div(t, w);
         seg[k] += (q >> b) * stride;
         if (b) off[k] |= (q & mk) << shift;
       }
@@ -189,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncPara
   const uint32_t w_off = bitlen32(red[0]), w_cnt = bitlen32(red[1]), w_del = bitlen32(red[2]);
   const uint32_t Ld = (U * w_del + 7) >> 3, Lc = (U * w_cnt + 7) >> 3, Lo = ((uint32_t)n * w_off + 7) >> 3;
   const uint32_t L = H + Ld + Lc + Lo;
-  if (tid == 0) st_release(&P.status[blk], (blk == 0 ? kFlagInc : kFlagAgg) | L);
+  if (tid == 0) st_relaxed(&P.status[blk], (blk == 0 ? kFlagInc : kFlagAgg) | L);
 
   // ---- 4. order the offsets: (segment rank, offset) composite ranks
   int path = 0;
@@ -301,19 +299,14 @@ __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncPara
   }
   __syncthreads();  // soff complete; union free for the stage
 
-  // ---- 5. warp 0: look-back | warps 1-7: bit-pack into the stage (payload byte 0 = stage byte 0)
+  // ---- 5. bit-pack into the stage (payload byte 0 = stage byte 0); the offset is not needed yet
   uint32_t* st = sm.u.stage;
-  if (wid == 0) {
-    const uint64_t ex = finish_lookback(P, blk, L);
-    if (lane == 0) {
-      sm.excl = ex;
-      atomicAdd(&R->path_blocks[path], 1ull);
-    }
-  } else {
-    const int t = tid - 32, nt = kThreads - 32;
+  if (tid == 0) atomicAdd(&R->path_blocks[path], 1ull);
+  {
+    const int t = tid, nt = kThreads;
     const uint32_t nwords = (L + 3) >> 2;
     for (uint32_t w = t; w < nwords; w += nt) st[w] = 0u;
-    named_sync(1, nt);
+    __syncthreads();
     if (t < 32) {
       // block header fields, one per lane (container.serialize_block, container.py:107-121)
       const int f = t;
@@ -374,8 +367,9 @@ __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncPara
   }
   __syncthreads();
 
-  // ---- 6. realigned vector stores of the payload
-  realign_copy(P.payload + sm.excl, st, L, tid, kThreads);
+  // ---- 6. decoupled look-back (whole CTA), then realigned vector stores
+  const uint64_t excl = finish_lookback(P, blk, L, sm.lb);
+  realign_copy(P.payload + excl, st, L, tid, kThreads);
 }
 
 }  // namespace gpzb
