@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_gpzb.so")
+LIB_PATH = os.environ.get("GPZB_LIB") or os.path.join(_HERE, "_gpzb.so")  # GPZB_LIB: A/B builds
 
 OK, DOMAIN, WIDTH, CORRUPT, UNSUPPORTED, INVALID = 0, 1, 2, 3, 4, 5
 F32, F64 = 0, 1

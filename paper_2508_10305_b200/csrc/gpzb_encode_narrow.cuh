@@ -27,12 +27,15 @@ namespace gpzb {
 #endif
 constexpr int kNarrowStageWords = 2048 + 32;  // narrow payload <= 7.7 KB
 
+template <int D, typename T>
 struct NarrowSmem {
-  uint64_t blk;
-  uint64_t excl;
+  uint64_t mbar[2];                     // one per prefetch buffer
+  uint64_t tick[2];                     // block id held by each buffer
   unsigned long long lb[2 * kWarps + 2];
   uint32_t red[kWarps * 4];
   uint32_t scan32[kWarps];
+  __align__(16) BlkRec rec[2];          // prefetched geometry records
+  __align__(16) T in[2][D][kMaxBs];     // prefetched inputs (bulk copies)
   __align__(16) uint32_t cnt[kMaxBs];   // run length per distinct segment rank
   __align__(16) uint32_t soff[kMaxBs];  // offsets in sorted order
   __align__(16) uint16_t uniq[kMaxBs];  // unique segment ids (Π N <= 2^16)
@@ -83,28 +86,28 @@ __device__ __forceinline__ uint64_t finish_lookback(const EncParams& P, uint64_t
   return excl;
 }
 
+// One block, all of K2's work for it.  `rec` and `in` point at the
+// prefetched copies in shared memory (`in` == nullptr: load directly).
 template <int D, bool F64>
-__global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncParams P) {
+__device__ __forceinline__ void encode_one(const EncParams& P,
+                                           NarrowSmem<D, typename std::conditional<F64, double, float>::type>& sm,
+                                           const uint64_t blk, const BlkRec* rec,
+                                           const typename std::conditional<F64, double, float>::type* in) {
   using T = typename std::conditional<F64, double, float>::type;
   constexpr int S = F64 ? 8 : 4;
   constexpr uint32_t H = 8 + D * (2 * S + 5) + 3;  // block header bytes (container.py:62-67)
-  __shared__ NarrowSmem sm;
   const int tid = threadIdx.x;
   DevResult* R = P.res;
-
-  if (tid == 0) sm.blk = atomicAdd(&R->ticket, 1ull);
-  __syncthreads();
-  const uint64_t blk = sm.blk;
-  const BlkRec* rec = P.rec + blk;
   const uint32_t kind = rec->kind;
   if (blk == 0 && tid == 32) write_global_header<D, F64>(P, R->eb_abs);
 
   if (kind != KIND_NARROW) {
     // wide (staged by K2w) or error block (size 0): look-back + copy only
-    const uint64_t L = (kind == KIND_WIDE) ? rec->side_len : 0ull;
+    const BlkRec* grec = P.rec + blk;  // side_len lives in global memory (written by K2w)
+    const uint64_t L = (kind == KIND_WIDE) ? grec->side_len : 0ull;
     if (tid == 0) st_relaxed(&P.status[blk], (blk == 0 ? kFlagInc : kFlagAgg) | L);
     const uint64_t ex = finish_lookback(P, blk, L, sm.lb);
-    if (L) realign_copy(P.payload + ex, reinterpret_cast<const uint32_t*>(P.side + rec->side_off),
+    if (L) realign_copy(P.payload + ex, reinterpret_cast<const uint32_t*>(P.side + grec->side_off),
                         (uint32_t)L, tid, kThreads);
     return;
   }
@@ -113,9 +116,28 @@ __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncPara
   const int n = (int)min((uint64_t)P.bs, P.count - first);
   const int p0 = tid * kItems;
 
-  // ---- 1. load + quantize to 32-bit (segment, offset)
+  // ---- 1. load (prefetched smem copy or direct) + quantize to 32-bit (segment, offset)
   T x[D][kItems];
-  load_particles<D, T>(P, first, n, p0, x);
+  if (in != nullptr) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      if (p0 < n) {
+        if constexpr (sizeof(T) == 4) {
+          const float4 v = *reinterpret_cast<const float4*>(in + a * kMaxBs + p0);
+          x[a][0] = v.x; x[a][1] = v.y; x[a][2] = v.z; x[a][3] = v.w;
+        } else {
+          const double2 v0 = *reinterpret_cast<const double2*>(in + a * kMaxBs + p0);
+          const double2 v1 = *reinterpret_cast<const double2*>(in + a * kMaxBs + p0 + 2);
+          x[a][0] = v0.x; x[a][1] = v0.y; x[a][2] = v1.x; x[a][3] = v1.y;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) x[a][k] = T(0);
+      }
+    }
+  } else {
+    load_particles<D, T>(P, first, n, p0, x);
+  }
   const uint32_t PN = rec->PN, sumb = rec->sumb;
   uint32_t seg[kItems], off[kItems];
 #pragma unroll
@@ -132,9 +154,9 @@ __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncPara
         // certified reciprocal quantizer (gpzb_common.cuh quantize_coord, mode 0)
         const double t = __dsub_rn((double)x[a][k], lo);
         const double r = __dmul_rn(t, rinv);
-        const uint32_t rl = (uint32_t)__double2loint(r), rh = (uint32_t)__double2hiint(r);
+        const uint32_t rl = (uint32_t)__double2loint(r);
         uint32_t q = (uint32_t)__double2loint(__dadd_rz(r, 4503599627370496.0));
-        if ((rl + 1u) <= 1u && (rl | rh) != 0u) q = exact_floor_div(t, w);
+        if ((rl + 1u) <= 1u) q = exact_floor_div(t, w);  // also taken (harmlessly) for t == 0
         seg[k] += (q >> b) * stride;
         if (b) off[k] |= (q & mk) << shift;
       }
@@ -370,6 +392,63 @@ __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncPara
   // ---- 6. decoupled look-back (whole CTA), then realigned vector stores
   const uint64_t excl = finish_lookback(P, blk, L, sm.lb);
   realign_copy(P.payload + excl, st, L, tid, kThreads);
+}
+
+// Persistent K2: grid = resident CTAs; blocks in ticket order.  Thread 0
+// keeps one ticket in reserve and bulk-copies the next block's record and
+// input into the other buffer while the current block is processed.
+template <int D, bool F64>
+__global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncParams P) {
+  using T = typename std::conditional<F64, double, float>::type;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  NarrowSmem<D, T>& sm = *reinterpret_cast<NarrowSmem<D, T>*>(smem_raw);
+  const int tid = threadIdx.x;
+  unsigned long long* ticket = &P.res->ticket;
+  const uint32_t in_bytes = (uint32_t)(D * P.bs * sizeof(T));
+
+  // issue the copies of block t into buffer b (thread 0)
+  auto issue = [&](uint64_t t, int b) {
+    const bool full = P.vec && (t + 1) * (uint64_t)P.bs <= P.count;
+    mbar_expect_tx(&sm.mbar[b], (uint32_t)sizeof(BlkRec) + (full ? in_bytes : 0u));
+    bulk_g2s(&sm.rec[b], P.rec + t, sizeof(BlkRec), &sm.mbar[b]);
+    if (full) {
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+        bulk_g2s(&sm.in[b][a][0], reinterpret_cast<const T*>(P.axes[a]) + t * P.bs,
+                 (uint32_t)(P.bs * sizeof(T)), &sm.mbar[b]);
+    }
+  };
+
+  unsigned long long pending = 0;
+  if (tid == 0) {
+    mbar_init(&sm.mbar[0], 1);
+    mbar_init(&sm.mbar[1], 1);
+    mbar_fence_init();
+    const unsigned long long t0 = atomicAdd(ticket, 1ull);
+    sm.tick[0] = t0;
+    if (t0 < P.nblocks) issue(t0, 0);
+    pending = atomicAdd(ticket, 1ull);
+  }
+  __syncthreads();
+  uint32_t parity[2] = {0u, 0u};
+  int cur = 0;
+  for (;;) {
+    const uint64_t t = sm.tick[cur];
+    if (t >= P.nblocks) break;
+    if (tid == 0) {  // next block into the other buffer (free since the last iteration)
+      sm.tick[cur ^ 1] = pending;
+      if (pending < P.nblocks) {
+        issue(pending, cur ^ 1);
+        pending = atomicAdd(ticket, 1ull);
+      }
+    }
+    mbar_wait(&sm.mbar[cur], parity[cur]);
+    parity[cur] ^= 1u;
+    const bool full = P.vec && (t + 1) * (uint64_t)P.bs <= P.count;
+    encode_one<D, F64>(P, sm, t, &sm.rec[cur], full ? &sm.in[cur][0][0] : nullptr);
+    __syncthreads();  // buffer `cur` and the scratch areas are free again
+    cur ^= 1;
+  }
 }
 
 }  // namespace gpzb

@@ -1,0 +1,15 @@
+#!/bin/bash
+# A/B: bench the default build and every build/*.so variant (compress/decompress GB/s only)
+cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
+mkdir -p gpurun_out
+for lib in paper_2508_10305_b200/_gpzb.so build/*.so; do
+  echo "== $lib" >> gpurun_out/ab.txt
+  GPZB_LIB=$PWD/$lib timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu 2>&1 | python -c "
+import json,sys
+for l in sys.stdin:
+    try: d=json.loads(l)
+    except Exception: print(l.strip()); continue
+    print('comp %.1f decomp %.1f k_encode %.3f k_decode %.3f k_range %.3f cr %.3f clk %s' % (d['value'], d['decompress']['value'], d['kernels']['k_encode_ms'], d['kernels']['k_decode_ms'], d['kernels']['k_range_ms'], d['compression_ratio'], d['clocks']))
+" >> gpurun_out/ab.txt
+done
+cat gpurun_out/ab.txt
