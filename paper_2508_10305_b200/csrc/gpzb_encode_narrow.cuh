@@ -86,10 +86,12 @@ __device__ __forceinline__ uint64_t finish_lookback(const EncParams& P, uint64_t
   return excl;
 }
 
-// One block, all of K2's work for it.  `rec` and `in` point at the
-// prefetched copies in shared memory (`in` == nullptr: load directly).
+// Front half of K2 for one block: everything up to the payload bytes in the
+// shared stage and the published aggregate.  Returns the payload length.
+// `rec` / `in` point at the prefetched shared copies (`in` == nullptr: load
+// directly from global memory).
 template <int D, bool F64>
-__device__ __forceinline__ void encode_one(const EncParams& P,
+__device__ __forceinline__ uint32_t encode_front(const EncParams& P,
                                            NarrowSmem<D, typename std::conditional<F64, double, float>::type>& sm,
                                            const uint64_t blk, const BlkRec* rec,
                                            const typename std::conditional<F64, double, float>::type* in) {
@@ -102,14 +104,10 @@ __device__ __forceinline__ void encode_one(const EncParams& P,
   if (blk == 0 && tid == 32) write_global_header<D, F64>(P, R->eb_abs);
 
   if (kind != KIND_NARROW) {
-    // wide (staged by K2w) or error block (size 0): look-back + copy only
-    const BlkRec* grec = P.rec + blk;  // side_len lives in global memory (written by K2w)
-    const uint64_t L = (kind == KIND_WIDE) ? grec->side_len : 0ull;
+    // wide (staged by K2w) or error block (size 0): aggregate only
+    const uint32_t L = (kind == KIND_WIDE) ? P.rec[blk].side_len : 0u;  // written by K2w
     if (tid == 0) st_relaxed(&P.status[blk], (blk == 0 ? kFlagInc : kFlagAgg) | L);
-    const uint64_t ex = finish_lookback(P, blk, L, sm.lb);
-    if (L) realign_copy(P.payload + ex, reinterpret_cast<const uint32_t*>(P.side + grec->side_off),
-                        (uint32_t)L, tid, kThreads);
-    return;
+    return L;
   }
 
   const uint64_t first = blk * (uint64_t)P.bs;
@@ -389,9 +387,19 @@ __device__ __forceinline__ void encode_one(const EncParams& P,
   }
   __syncthreads();
 
-  // ---- 6. decoupled look-back (whole CTA), then realigned vector stores
+  return L;
+}
+
+// Back half: decoupled look-back (whole CTA), table entry, and the payload's
+// realigned vector stores from the stage (narrow) or the side buffer (wide).
+template <int D, typename T>
+__device__ __forceinline__ void encode_back(const EncParams& P, NarrowSmem<D, T>& sm, uint64_t blk, uint32_t L,
+                                            bool narrow) {
   const uint64_t excl = finish_lookback(P, blk, L, sm.lb);
-  realign_copy(P.payload + excl, st, L, tid, kThreads);
+  if (!L) return;
+  if (narrow) realign_copy(P.payload + excl, sm.u.stage, L, threadIdx.x, kThreads);
+  else realign_copy(P.payload + excl, reinterpret_cast<const uint32_t*>(P.side + P.rec[blk].side_off), L,
+                    threadIdx.x, kThreads);
 }
 
 // Persistent K2: grid = resident CTAs; blocks in ticket order.  Thread 0
@@ -419,7 +427,6 @@ __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncPara
     }
   };
 
-  unsigned long long pending = 0;
   if (tid == 0) {
     mbar_init(&sm.mbar[0], 1);
     mbar_init(&sm.mbar[1], 1);
@@ -427,26 +434,30 @@ __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncPara
     const unsigned long long t0 = atomicAdd(ticket, 1ull);
     sm.tick[0] = t0;
     if (t0 < P.nblocks) issue(t0, 0);
-    pending = atomicAdd(ticket, 1ull);
   }
   __syncthreads();
   uint32_t parity[2] = {0u, 0u};
   int cur = 0;
+  uint64_t prev = ~0ull;  // block whose back half is still pending
+  uint32_t prev_len = 0;
+  bool prev_narrow = false;
   for (;;) {
     const uint64_t t = sm.tick[cur];
+    unsigned long long tn = 0;
+    if (tid == 0 && t < P.nblocks) tn = atomicAdd(ticket, 1ull);  // consumed after the back half
+    if (prev != ~0ull) encode_back<D, T>(P, sm, prev, prev_len, prev_narrow);
     if (t >= P.nblocks) break;
-    if (tid == 0) {  // next block into the other buffer (free since the last iteration)
-      sm.tick[cur ^ 1] = pending;
-      if (pending < P.nblocks) {
-        issue(pending, cur ^ 1);
-        pending = atomicAdd(ticket, 1ull);
-      }
+    if (tid == 0) {
+      sm.tick[cur ^ 1] = tn;
+      if (tn < P.nblocks) issue(tn, cur ^ 1);  // buffer cur^1 was consumed last iteration
     }
     mbar_wait(&sm.mbar[cur], parity[cur]);
     parity[cur] ^= 1u;
     const bool full = P.vec && (t + 1) * (uint64_t)P.bs <= P.count;
-    encode_one<D, F64>(P, sm, t, &sm.rec[cur], full ? &sm.in[cur][0][0] : nullptr);
-    __syncthreads();  // buffer `cur` and the scratch areas are free again
+    prev_narrow = sm.rec[cur].kind == KIND_NARROW;
+    prev_len = encode_front<D, F64>(P, sm, t, &sm.rec[cur], full ? &sm.in[cur][0][0] : nullptr);
+    prev = t;
+    __syncthreads();  // stage complete; tick[cur ^ 1] visible
     cur ^= 1;
   }
 }
