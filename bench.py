@@ -48,6 +48,7 @@ def parse_args():
     p.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--compress-only", action="store_true", help="experiments: skip decompress")
     return p.parse_args()
 
 
@@ -218,7 +219,9 @@ def main():
             else:
                 cont = gz.compress_device(ds, cfg, timing=timing)
             b.record()
-            if world > 1:
+            if args.compress_only:
+                rec = None
+            elif world > 1:
                 rec = sharded.decompress_device(cont, timing=timing)
             else:
                 rec = gz.decompress_device(cont, timing=timing)
@@ -290,6 +293,7 @@ def main():
         traffic = tj.get("encode", {}).get("dram_bytes_per_launch")
     enc_avg = statistics.mean(enc_ms) / 1e3 if enc_ms else float("nan")
     dec_avg = statistics.mean(dec_ms) / 1e3 if dec_ms else float("nan")
+    t_d = t_d or float("nan")
     rng_avg = statistics.mean(rng_ms) / 1e3 if rng_ms else float("nan")
     roof = {"bound": "hbm", "kernel": "k_encode (K2)", "achieved": enc_bytes / enc_avg / 1e9, "peak": hbm,
             "unit": "GB/s", "frac": enc_bytes / enc_avg / 1e9 / hbm, "traffic": traffic,

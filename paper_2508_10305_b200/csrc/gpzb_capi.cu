@@ -103,18 +103,7 @@ void launch_encode(const EncParams& P, bool wide, cudaStream_t s) {
     if (P.preserve) k_encode_wide<D, F64, true><<<grid, kThreads, 0, s>>>(P);
     else k_encode_wide<D, F64, false><<<grid, kThreads, 0, s>>>(P);
   }
-  using T = typename std::conditional<F64, double, float>::type;
-  const int smem = (int)sizeof(NarrowSmem<D, T>);
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_encode<D, F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_set = true;
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_encode<D, F64>, kThreads, smem);
-  if (per_sm < 1) per_sm = 1;
-  const uint64_t grid = std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * per_sm);
-  k_encode<D, F64><<<(unsigned)grid, kThreads, smem, s>>>(P);
+  k_encode<D, F64><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
 }
 
 template <int D, bool F64>

@@ -163,16 +163,22 @@ __device__ __forceinline__ T block_excl_scan(T v, T& total, T* ws) {
   }
   if (lane == 31) ws[wid] = x;
   __syncthreads();
-  T pre = 0, tot = 0;
+  // every warp scans the kWarps totals itself (lanes 0..kWarps-1)
+  T s = (lane < kWarps) ? ws[lane] : T(0);
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    T s = ws[w];
-    pre += (w < wid) ? s : T(0);
-    tot += s;
+  for (int o = 1; o < kWarps; o <<= 1) {
+    T y = __shfl_up_sync(kFull, s, o);
+    if (lane >= o) s += y;
   }
-  total = tot;
+  const T incl_w = __shfl_sync(kFull, s, wid);          // inclusive through this warp
+  total = __shfl_sync(kFull, s, kWarps - 1);
   __syncthreads();
-  return pre + x - v;
+  return incl_w - __shfl_sync(kFull, x, 31) + x - v;  // exclusive prefix of this thread
+}
+
+// Shared-memory atomic OR without a returned value (RED, no scoreboard wait).
+__device__ __forceinline__ void red_or_shared(uint32_t* p, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
 // OR-reduction over the CTA of NV u32 values; result broadcast to all.
@@ -317,9 +323,9 @@ __device__ __forceinline__ void or_bits(uint32_t* st, uint64_t pos, uint64_t v) 
   const uint64_t lo = v << sh;
   const uint32_t w0 = (uint32_t)lo, w1 = (uint32_t)(lo >> 32);
   const uint32_t w2 = sh ? (uint32_t)(v >> (64 - sh)) : 0u;
-  if (w0) atomicOr(w, w0);
-  if (w1) atomicOr(w + 1, w1);
-  if (w2) atomicOr(w + 2, w2);
+  if (w0) red_or_shared(w, w0);
+  if (w1) red_or_shared(w + 1, w1);
+  if (w2) red_or_shared(w + 2, w2);
 }
 
 // Read `nbits` (<= 64) bits at bit position pos from a u32 word array.

@@ -293,20 +293,28 @@ __global__ void __launch_bounds__(256) k_geometry(const EncParams P) {
 // --------------------------------------------------- shared K2 building blocks
 // Bitmap rank machinery: zero / set / prefix.  Words [0, nw) of bm, prefix
 // counts into wp.  bm_prefix returns the number of set bits.
+// bm must be 16B aligned and sized to a multiple of 4 words >= nw.
 __device__ __forceinline__ void bm_zero(uint32_t* bm, int nw) {
-  for (int w = threadIdx.x; w < nw; w += kThreads) bm[w] = 0u;
+  for (int w = threadIdx.x; w < (nw + 3) >> 2; w += kThreads) reinterpret_cast<uint4*>(bm)[w] = make_uint4(0, 0, 0, 0);
 }
+// Each thread owns a run of whole uint4 groups of words.
 __device__ __forceinline__ uint32_t bm_prefix(const uint32_t* bm, uint16_t* wp, int nw, uint32_t* scan_ws) {
-  const int wpt = (nw + kThreads - 1) / kThreads;
-  const int w0 = threadIdx.x * wpt;
-  const int w1 = min(w0 + wpt, nw);
+  const int ng = (nw + 3) >> 2;
+  const int gpt = (ng + kThreads - 1) / kThreads;
+  const int g0 = threadIdx.x * gpt;
+  const int g1 = min(g0 + gpt, ng);
   uint32_t local = 0;
-  for (int w = w0; w < w1; ++w) local += __popc(bm[w]);
+  for (int g = g0; g < g1; ++g) {
+    const uint4 q = reinterpret_cast<const uint4*>(bm)[g];
+    local += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+  }
   uint32_t total;
   uint32_t run = block_excl_scan<uint32_t>(local, total, scan_ws);
-  for (int w = w0; w < w1; ++w) {
-    wp[w] = (uint16_t)run;
-    run += __popc(bm[w]);
+  for (int g = g0; g < g1; ++g) {
+    const uint4 q = reinterpret_cast<const uint4*>(bm)[g];
+    const uint32_t a = run, b = a + __popc(q.x), c = b + __popc(q.y), d = c + __popc(q.z);
+    reinterpret_cast<uint2*>(wp)[g] = make_uint2(a | (b << 16), c | (d << 16));
+    run = d + __popc(q.w);
   }
   return total;
 }
@@ -327,7 +335,7 @@ __device__ __forceinline__ void lsd_ranks(const uint32_t (&digit)[kItems], int d
   for (int k = 0; k < kItems; ++k)
     if (p0 + k < n) {
       uint32_t c = (digit[k] << 10) | (uint32_t)(p0 + k);
-      atomicOr(&bm[c >> 5], 1u << (c & 31));
+      red_or_shared(&bm[c >> 5], 1u << (c & 31));
     }
   __syncthreads();
   bm_prefix(bm, wp, nw, scan_ws);

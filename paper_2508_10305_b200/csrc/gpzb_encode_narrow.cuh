@@ -23,22 +23,19 @@
 namespace gpzb {
 
 #ifndef GPZB_K2_MINB
-#define GPZB_K2_MINB 4
+#define GPZB_K2_MINB 7
 #endif
 constexpr int kNarrowStageWords = 2048 + 32;  // narrow payload <= 7.7 KB
 
-template <int D, typename T>
 struct NarrowSmem {
-  uint64_t mbar[2];                     // one per prefetch buffer
-  uint64_t tick[2];                     // block id held by each buffer
+  uint64_t blk;
+  uint64_t excl;
   unsigned long long lb[2 * kWarps + 2];
   uint32_t red[kWarps * 4];
   uint32_t scan32[kWarps];
-  __align__(16) BlkRec rec[2];          // prefetched geometry records
-  __align__(16) T in[2][D][kMaxBs];     // prefetched inputs (bulk copies)
   __align__(16) uint32_t cnt[kMaxBs];   // run length per distinct segment rank
   __align__(16) uint32_t soff[kMaxBs];  // offsets in sorted order
-  __align__(16) uint16_t uniq[kMaxBs];  // unique segment ids (Π N <= 2^16)
+  __align__(16) uint16_t uniqp[kMaxBs + 8];  // [0] = 0 sentinel, [r + 1] = unique id r (Π N <= 2^16)
   union U {
     struct { uint32_t bm[2048]; uint16_t wp[2048]; } a;
     struct { uint32_t bm[2048]; uint16_t wp[2048]; uint32_t cnt2[kMaxBs]; } b;
@@ -76,7 +73,11 @@ __device__ void write_global_header(const EncParams& P, double eb_abs) {
 // already published); publishes the inclusive prefix and the table entry.
 __device__ __forceinline__ uint64_t finish_lookback(const EncParams& P, uint64_t blk, uint64_t L,
                                                     unsigned long long* ws) {
+#ifdef GPZB_NO_LOOKBACK  // experiment builds only: measures K2 without the scan (wrong container)
+  const uint64_t excl = (blk * 1600ull) % (64ull << 20);
+#else
   const uint64_t excl = blk ? lookback_cta(P.status, blk, ws) : 0ull;
+#endif
   const int tid = threadIdx.x;
   if (tid == 0) {
     if (blk > 0) st_relaxed(&P.status[blk], kFlagInc | (excl + L));
@@ -86,51 +87,33 @@ __device__ __forceinline__ uint64_t finish_lookback(const EncParams& P, uint64_t
   return excl;
 }
 
-// Front half of K2 for one block: everything up to the payload bytes in the
-// shared stage and the published aggregate.  Returns the payload length.
-// `rec` / `in` point at the prefetched shared copies (`in` == nullptr: load
-// directly from global memory).
-template <int D, bool F64>
-__device__ __forceinline__ uint32_t encode_front(const EncParams& P,
-                                           NarrowSmem<D, typename std::conditional<F64, double, float>::type>& sm,
-                                           const uint64_t blk, const BlkRec* rec,
-                                           const typename std::conditional<F64, double, float>::type* in) {
+// The narrow-block work, specialised for full 1024-particle blocks (FULL:
+// no per-particle bounds predicates) and for the partial tail block.
+template <int D, bool F64, bool FULL>
+__device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, const uint64_t blk,
+                                            const BlkRec* rec, const int n) {
   using T = typename std::conditional<F64, double, float>::type;
   constexpr int S = F64 ? 8 : 4;
   constexpr uint32_t H = 8 + D * (2 * S + 5) + 3;  // block header bytes (container.py:62-67)
   const int tid = threadIdx.x;
   DevResult* R = P.res;
-  const uint32_t kind = rec->kind;
-  if (blk == 0 && tid == 32) write_global_header<D, F64>(P, R->eb_abs);
-
-  if (kind != KIND_NARROW) {
-    // wide (staged by K2w) or error block (size 0): aggregate only
-    const uint32_t L = (kind == KIND_WIDE) ? P.rec[blk].side_len : 0u;  // written by K2w
-    if (tid == 0) st_relaxed(&P.status[blk], (blk == 0 ? kFlagInc : kFlagAgg) | L);
-    return L;
-  }
-
   const uint64_t first = blk * (uint64_t)P.bs;
-  const int n = (int)min((uint64_t)P.bs, P.count - first);
   const int p0 = tid * kItems;
+#define VALID(k) (FULL || p0 + (k) < n)
 
-  // ---- 1. load (prefetched smem copy or direct) + quantize to 32-bit (segment, offset)
+  // ---- 1. load + quantize to 32-bit (segment, offset)
   T x[D][kItems];
-  if (in != nullptr) {
+  if constexpr (FULL) {
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      if (p0 < n) {
-        if constexpr (sizeof(T) == 4) {
-          const float4 v = *reinterpret_cast<const float4*>(in + a * kMaxBs + p0);
-          x[a][0] = v.x; x[a][1] = v.y; x[a][2] = v.z; x[a][3] = v.w;
-        } else {
-          const double2 v0 = *reinterpret_cast<const double2*>(in + a * kMaxBs + p0);
-          const double2 v1 = *reinterpret_cast<const double2*>(in + a * kMaxBs + p0 + 2);
-          x[a][0] = v0.x; x[a][1] = v0.y; x[a][2] = v1.x; x[a][3] = v1.y;
-        }
+      const T* base = reinterpret_cast<const T*>(P.axes[a]) + first + p0;
+      if constexpr (sizeof(T) == 4) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(base));
+        x[a][0] = v.x; x[a][1] = v.y; x[a][2] = v.z; x[a][3] = v.w;
       } else {
-#pragma unroll
-        for (int k = 0; k < kItems; ++k) x[a][k] = T(0);
+        const double2 v0 = __ldcs(reinterpret_cast<const double2*>(base));
+        const double2 v1 = __ldcs(reinterpret_cast<const double2*>(base) + 1);
+        x[a][0] = v0.x; x[a][1] = v0.y; x[a][2] = v1.x; x[a][3] = v1.y;
       }
     }
   } else {
@@ -141,39 +124,63 @@ __device__ __forceinline__ uint32_t encode_front(const EncParams& P,
 #pragma unroll
   for (int k = 0; k < kItems; ++k) { seg[k] = 0; off[k] = 0; }
   {
+    // certified reciprocal quantizer (gpzb_common.cuh quantize_coord, mode 0);
+    // coordinates whose certificate fails are redone exactly in one
+    // warp-uniform pass (rare: t == 0 or RN(t/w) within an ulp of an integer)
+    uint32_t redo = 0;
     uint32_t stride = 1, shift = 0;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      const double lo = rec->lo[a], rinv = rec->rinv[a], w = rec->w[a];
+      const double lo = rec->lo[a], rinv = rec->rinv[a];
       const uint32_t b = rec->b[a];
       const uint32_t mk = (1u << b) - 1u;
 #pragma unroll
       for (int k = 0; k < kItems; ++k) {
-        // certified reciprocal quantizer (gpzb_common.cuh quantize_coord, mode 0)
         const double t = __dsub_rn((double)x[a][k], lo);
         const double r = __dmul_rn(t, rinv);
-        const uint32_t rl = (uint32_t)__double2loint(r);
-        uint32_t q = (uint32_t)__double2loint(__dadd_rz(r, 4503599627370496.0));
-        if ((rl + 1u) <= 1u) q = exact_floor_div(t, w);  // also taken (harmlessly) for t == 0
+        const uint32_t rl = (uint32_t)__double2loint(r), rh = (uint32_t)__double2hiint(r);
+        const uint32_t q = (uint32_t)__double2loint(__dadd_rz(r, 4503599627370496.0));
+        redo |= ((rl + 1u) <= 1u && (rl | rh) != 0u) ? (1u << k) : 0u;  // r == 0 is exact
         seg[k] += (q >> b) * stride;
-        if (b) off[k] |= (q & mk) << shift;
+        off[k] |= (q & mk) << (shift & 31);  // b == 0 -> mk == 0
       }
       stride *= rec->N[a];
       shift += b;
     }
+    if (__any_sync(kFull, redo != 0)) {
+      // re-linearise the affected particles with exact division where the
+      // certificate failed (identical result wherever it held)
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        if (!(redo & (1u << k))) continue;
+        uint32_t sk = 0, ok = 0, st = 1, sh = 0;
+        for (int a = 0; a < D; ++a) {
+          const double t = __dsub_rn((double)x[a][k], rec->lo[a]);
+          const uint32_t q = exact_floor_div(t, rec->w[a]);
+          const uint32_t b = rec->b[a];
+          sk += (q >> b) * st;
+          ok |= (q & ((1u << b) - 1u)) << (sh & 31);
+          st *= rec->N[a];
+          sh += b;
+        }
+        seg[k] = sk;
+        off[k] = ok;
+      }
+    }
   }
   uint32_t off_or = 0;
 #pragma unroll
-  for (int k = 0; k < kItems; ++k) off_or |= (p0 + k < n) ? off[k] : 0u;
+  for (int k = 0; k < kItems; ++k) off_or |= VALID(k) ? off[k] : 0u;
 
   // ---- 2. pass A: distinct-segment ranks, run lengths, unique ids
   const int nwA = (int)((PN + 31) >> 5);
   bm_zero(sm.u.a.bm, nwA);
   reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(0, 0, 0, 0);
+  if (tid == 0) sm.uniqp[0] = 0;
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < kItems; ++k)
-    if (p0 + k < n) atomicOr(&sm.u.a.bm[seg[k] >> 5], 1u << (seg[k] & 31));
+    if (VALID(k)) red_or_shared(&sm.u.a.bm[seg[k] >> 5], 1u << (seg[k] & 31));
   __syncthreads();
   const uint32_t U = bm_prefix(sm.u.a.bm, sm.u.a.wp, nwA, sm.scan32);
   __syncthreads();
@@ -181,10 +188,10 @@ __device__ __forceinline__ uint32_t encode_front(const EncParams& P,
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
     srank[k] = tie[k] = 0;
-    if (p0 + k < n) {
+    if (VALID(k)) {
       srank[k] = bm_rank(sm.u.a.bm, sm.u.a.wp, seg[k]);
       tie[k] = atomicAdd(&sm.cnt[srank[k]], 1u);
-      sm.uniq[srank[k]] = (uint16_t)seg[k];
+      sm.uniqp[srank[k] + 1] = (uint16_t)seg[k];
     }
   }
   __syncthreads();
@@ -198,7 +205,7 @@ __device__ __forceinline__ uint32_t encode_front(const EncParams& P,
     if (r < U) {
       cloc[j] = sm.cnt[r];
       c_or |= cloc[j];
-      d_or |= (uint32_t)sm.uniq[r] - (r ? (uint32_t)sm.uniq[r - 1] : 0u);
+      d_or |= (uint32_t)sm.uniqp[r + 1] - (uint32_t)sm.uniqp[r];
       csum += cloc[j];
     }
   }
@@ -213,7 +220,7 @@ __device__ __forceinline__ uint32_t encode_front(const EncParams& P,
   int path = 0;
   if (w_off) {
     uint32_t pos[kItems];
-    if (sumb <= 16 && (U << sumb) <= 65536u) {
+    if (w_cnt > 3 && sumb <= 16 && (U << sumb) <= 65536u) {
       path = 1;
       const int nw = (int)(((U << sumb) + 31) >> 5);
       bm_zero(sm.u.b.bm, nw);
@@ -223,7 +230,7 @@ __device__ __forceinline__ uint32_t encode_front(const EncParams& P,
 #pragma unroll
       for (int k = 0; k < kItems; ++k) {
         c[k] = (srank[k] << sumb) | off[k];
-        if (p0 + k < n) atomicOr(&sm.u.b.bm[c[k] >> 5], 1u << (c[k] & 31));
+        if VALID(k) red_or_shared(&sm.u.b.bm[c[k] >> 5], 1u << (c[k] & 31));
       }
       __syncthreads();
       const uint32_t nd = bm_prefix(sm.u.b.bm, sm.u.b.wp, nw, sm.scan32);
@@ -232,7 +239,7 @@ __device__ __forceinline__ uint32_t encode_front(const EncParams& P,
 #pragma unroll
       for (int k = 0; k < kItems; ++k) {
         cr[k] = t2[k] = 0;
-        if (p0 + k < n) {
+        if VALID(k) {
           cr[k] = bm_rank(sm.u.b.bm, sm.u.b.wp, c[k]);
           t2[k] = atomicAdd(&sm.u.b.cnt2[cr[k]], 1u);
         }
@@ -253,7 +260,7 @@ __device__ __forceinline__ uint32_t encode_front(const EncParams& P,
       }
       __syncthreads();
 #pragma unroll
-      for (int k = 0; k < kItems; ++k) pos[k] = (p0 + k < n) ? sm.u.b.cnt2[cr[k]] + t2[k] : 0u;
+      for (int k = 0; k < kItems; ++k) pos[k] = VALID(k) ? sm.u.b.cnt2[cr[k]] + t2[k] : 0u;
     } else if (w_cnt <= 6) {
       // segment groups of <= 63 particles: rank by comparison inside the group
       path = 2;
@@ -269,7 +276,7 @@ __device__ __forceinline__ uint32_t encode_front(const EncParams& P,
 #pragma unroll
       for (int k = 0; k < kItems; ++k) {
         g0[k] = 0;
-        if (p0 + k < n) {
+        if VALID(k) {
           g0[k] = sm.u.c.segstart[srank[k]];
           sm.u.c.tmp[g0[k] + tie[k]] = off[k];
         }
@@ -278,7 +285,7 @@ __device__ __forceinline__ uint32_t encode_front(const EncParams& P,
 #pragma unroll
       for (int k = 0; k < kItems; ++k) {
         pos[k] = 0;
-        if (p0 + k < n) {
+        if VALID(k) {
           const uint32_t gs = sm.cnt[srank[k]], me = g0[k] + tie[k];
           uint32_t rr = 0;
           for (uint32_t j = g0[k]; j < g0[k] + gs; ++j) {
@@ -315,7 +322,7 @@ __device__ __forceinline__ uint32_t encode_front(const EncParams& P,
     }
 #pragma unroll
     for (int k = 0; k < kItems; ++k)
-      if (p0 + k < n) sm.soff[pos[k]] = off[k];
+      if VALID(k) sm.soff[pos[k]] = off[k];
   }
   __syncthreads();  // soff complete; union free for the stage
 
@@ -324,8 +331,8 @@ __device__ __forceinline__ uint32_t encode_front(const EncParams& P,
   if (tid == 0) atomicAdd(&R->path_blocks[path], 1ull);
   {
     const int t = tid, nt = kThreads;
-    const uint32_t nwords = (L + 3) >> 2;
-    for (uint32_t w = t; w < nwords; w += nt) st[w] = 0u;
+    const uint32_t nquads = (L + 15) >> 4;
+    for (uint32_t w = t; w < nquads; w += nt) reinterpret_cast<uint4*>(st)[w] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     if (t < 32) {
       // block header fields, one per lane (container.serialize_block, container.py:107-121)
@@ -363,7 +370,7 @@ __device__ __forceinline__ uint32_t encode_front(const EncParams& P,
       for (int j = 0; j < 4; ++j) {
         const uint32_t r = r0 + j;
         if (r < U) {
-          const uint32_t d = (uint32_t)sm.uniq[r] - (r ? (uint32_t)sm.uniq[r - 1] : 0u);
+          const uint32_t d = (uint32_t)sm.uniqp[r + 1] - (uint32_t)sm.uniqp[r];
           dv |= (uint64_t)d << (j * w_del);
           cv |= (uint64_t)sm.cnt[r] << (j * w_cnt);
         }
@@ -387,79 +394,39 @@ __device__ __forceinline__ uint32_t encode_front(const EncParams& P,
   }
   __syncthreads();
 
-  return L;
-}
-
-// Back half: decoupled look-back (whole CTA), table entry, and the payload's
-// realigned vector stores from the stage (narrow) or the side buffer (wide).
-template <int D, typename T>
-__device__ __forceinline__ void encode_back(const EncParams& P, NarrowSmem<D, T>& sm, uint64_t blk, uint32_t L,
-                                            bool narrow) {
+  // ---- 6. decoupled look-back (whole CTA), then realigned vector stores
   const uint64_t excl = finish_lookback(P, blk, L, sm.lb);
-  if (!L) return;
-  if (narrow) realign_copy(P.payload + excl, sm.u.stage, L, threadIdx.x, kThreads);
-  else realign_copy(P.payload + excl, reinterpret_cast<const uint32_t*>(P.side + P.rec[blk].side_off), L,
-                    threadIdx.x, kThreads);
+  realign_copy(P.payload + excl, st, L, tid, kThreads);
+#undef VALID
 }
 
-// Persistent K2: grid = resident CTAs; blocks in ticket order.  Thread 0
-// keeps one ticket in reserve and bulk-copies the next block's record and
-// input into the other buffer while the current block is processed.
 template <int D, bool F64>
 __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncParams P) {
-  using T = typename std::conditional<F64, double, float>::type;
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  NarrowSmem<D, T>& sm = *reinterpret_cast<NarrowSmem<D, T>*>(smem_raw);
+  __shared__ NarrowSmem sm;
   const int tid = threadIdx.x;
-  unsigned long long* ticket = &P.res->ticket;
-  const uint32_t in_bytes = (uint32_t)(D * P.bs * sizeof(T));
+  DevResult* R = P.res;
 
-  // issue the copies of block t into buffer b (thread 0)
-  auto issue = [&](uint64_t t, int b) {
-    const bool full = P.vec && (t + 1) * (uint64_t)P.bs <= P.count;
-    mbar_expect_tx(&sm.mbar[b], (uint32_t)sizeof(BlkRec) + (full ? in_bytes : 0u));
-    bulk_g2s(&sm.rec[b], P.rec + t, sizeof(BlkRec), &sm.mbar[b]);
-    if (full) {
-#pragma unroll
-      for (int a = 0; a < D; ++a)
-        bulk_g2s(&sm.in[b][a][0], reinterpret_cast<const T*>(P.axes[a]) + t * P.bs,
-                 (uint32_t)(P.bs * sizeof(T)), &sm.mbar[b]);
-    }
-  };
-
-  if (tid == 0) {
-    mbar_init(&sm.mbar[0], 1);
-    mbar_init(&sm.mbar[1], 1);
-    mbar_fence_init();
-    const unsigned long long t0 = atomicAdd(ticket, 1ull);
-    sm.tick[0] = t0;
-    if (t0 < P.nblocks) issue(t0, 0);
-  }
+  if (tid == 0) sm.blk = atomicAdd(&R->ticket, 1ull);
   __syncthreads();
-  uint32_t parity[2] = {0u, 0u};
-  int cur = 0;
-  uint64_t prev = ~0ull;  // block whose back half is still pending
-  uint32_t prev_len = 0;
-  bool prev_narrow = false;
-  for (;;) {
-    const uint64_t t = sm.tick[cur];
-    unsigned long long tn = 0;
-    if (tid == 0 && t < P.nblocks) tn = atomicAdd(ticket, 1ull);  // consumed after the back half
-    if (prev != ~0ull) encode_back<D, T>(P, sm, prev, prev_len, prev_narrow);
-    if (t >= P.nblocks) break;
-    if (tid == 0) {
-      sm.tick[cur ^ 1] = tn;
-      if (tn < P.nblocks) issue(tn, cur ^ 1);  // buffer cur^1 was consumed last iteration
-    }
-    mbar_wait(&sm.mbar[cur], parity[cur]);
-    parity[cur] ^= 1u;
-    const bool full = P.vec && (t + 1) * (uint64_t)P.bs <= P.count;
-    prev_narrow = sm.rec[cur].kind == KIND_NARROW;
-    prev_len = encode_front<D, F64>(P, sm, t, &sm.rec[cur], full ? &sm.in[cur][0][0] : nullptr);
-    prev = t;
-    __syncthreads();  // stage complete; tick[cur ^ 1] visible
-    cur ^= 1;
+  const uint64_t blk = sm.blk;
+  const BlkRec* rec = P.rec + blk;
+  const uint32_t kind = rec->kind;
+  if (blk == 0 && tid == 32) write_global_header<D, F64>(P, R->eb_abs);
+
+  if (kind != KIND_NARROW) {
+    // wide (staged by K2w) or error block (size 0): look-back + copy only
+    const uint64_t L = (kind == KIND_WIDE) ? rec->side_len : 0ull;
+    if (tid == 0) st_relaxed(&P.status[blk], (blk == 0 ? kFlagInc : kFlagAgg) | L);
+    const uint64_t ex = finish_lookback(P, blk, L, sm.lb);
+    if (L) realign_copy(P.payload + ex, reinterpret_cast<const uint32_t*>(P.side + rec->side_off),
+                        (uint32_t)L, tid, kThreads);
+    return;
   }
+
+  const uint64_t first = blk * (uint64_t)P.bs;
+  const int n = (int)min((uint64_t)P.bs, P.count - first);
+  if (n == kMaxBs && P.vec) narrow_body<D, F64, true>(P, sm, blk, rec, n);
+  else narrow_body<D, F64, false>(P, sm, blk, rec, n);
 }
 
 }  // namespace gpzb

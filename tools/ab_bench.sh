@@ -4,7 +4,7 @@ cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
 for lib in paper_2508_10305_b200/_gpzb.so build/*.so; do
   echo "== $lib" >> gpurun_out/ab.txt
-  GPZB_LIB=$PWD/$lib timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu 2>&1 | python -c "
+  GPZB_LIB=$PWD/$lib timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu $AB_ARGS 2>&1 | python -c "
 import json,sys
 for l in sys.stdin:
     try: d=json.loads(l)
