@@ -108,8 +108,14 @@ void launch_encode(const EncParams& P, bool wide, cudaStream_t s) {
 
 template <int D, bool F64>
 void launch_decode(const DecParams& P, bool pres, cudaStream_t s) {
-  if (pres) k_decode<D, F64, true><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
-  else k_decode<D, F64, false><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
+  const unsigned pgrid = (unsigned)((P.nblocks + 255) / 256);
+  if (pres) {
+    k_decode_plan<D, F64, true><<<pgrid, 256, 0, s>>>(P);
+    k_decode<D, F64, true><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
+  } else {
+    k_decode_plan<D, F64, false><<<pgrid, 256, 0, s>>>(P);
+    k_decode<D, F64, false><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
+  }
 }
 
 #define DISPATCH_DP(dims, prec, FN, ...)                      \
@@ -225,8 +231,7 @@ int gpzb_compress_workspace(uint64_t count, int dims, int prec, uint32_t bs, uin
 }
 
 int gpzb_decompress_workspace(const gpzb_header* h, uint64_t* ws_bytes) {
-  (void)h;
-  *ws_bytes = align_up(sizeof(DevResult));
+  *ws_bytes = align_up(sizeof(DevResult)) + align_up(h->block_count * sizeof(DecRec));
   return GPZB_OK;
 }
 
@@ -451,6 +456,8 @@ int gpzb_decompress_async(const uint8_t* c, uint64_t len, const gpzb_header* h, 
   P.out_cap = out_cap;
   P.out_offsets = out_offsets;
   P.res = reinterpret_cast<DevResult*>(ws);
+  if (ws_bytes < align_up(sizeof(DevResult)) + h->block_count * sizeof(DecRec)) return GPZB_INVALID_ARGUMENT;
+  P.rec = reinterpret_cast<DecRec*>(static_cast<uint8_t*>(ws) + align_up(sizeof(DevResult)));
   DISPATCH_DP(h->dims, h->precision, launch_decode, P, h->preserve_order != 0, s);
   return cuda_status(cudaGetLastError());
 }
