@@ -8,8 +8,8 @@ timeout 600 python bench.py --steps 2 --warmup 1 --particles 10000000 --no-cpu >
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/bench_ncu.json 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_encode -s 2 -c 1 -o gpurun_out/prof_encode -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_encode$" -s 2 -c 1 -o gpurun_out/prof_encode -f \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_encode.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_decode -s 2 -c 1 -o gpurun_out/prof_decode -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_decode$" -s 2 -c 1 -o gpurun_out/prof_decode -f \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_decode.log 2>&1
 ls -la gpurun_out
