@@ -330,6 +330,9 @@ def main():
         "roofline": roof,
         "step_roofline": step_roof,
         "kernels": {"k_range_ms": rng_avg * 1e3,
+                    "per_dataset_ms": {k: [statistics.mean(v[i::len(datasets)]) if v else None
+                                           for i in range(len(datasets))]
+                                       for k, v in (("k_encode", enc_ms), ("k_decode", dec_ms), ("k_range", rng_ms))},
                     "k_range_gbps": local_in / rng_avg / 1e9 if rng_ms else None,
                     "k_encode_ms": enc_avg * 1e3, "k_decode_ms": dec_avg * 1e3},
         "gpu_launches": len(enc_ms) + len(dec_ms) + len(rng_ms),

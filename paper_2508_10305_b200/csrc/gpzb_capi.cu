@@ -20,7 +20,7 @@ constexpr uint64_t kAlign = 256;
 inline uint64_t align_up(uint64_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
 
 struct EncLayout {
-  uint64_t status, bounds, rec, list, total;
+  uint64_t status, tstat, bounds, rec, list, staging, total;
 };
 
 inline uint64_t nblocks_of(uint64_t count, uint32_t bs) { return bs ? (count + bs - 1) / bs : 0; }
@@ -28,10 +28,12 @@ inline uint64_t nblocks_of(uint64_t count, uint32_t bs) { return bs ? (count + b
 EncLayout enc_layout(uint64_t nblocks, int dims, int prec) {
   EncLayout L;
   L.status = align_up(sizeof(DevResult));
-  L.bounds = align_up(L.status + 8 * nblocks);
+  L.tstat = align_up(L.status + 8 * nblocks);
+  L.bounds = align_up(L.tstat + 8 * ((nblocks + kScanTile - 1) / kScanTile));
   L.rec = align_up(L.bounds + nblocks * 2ull * dims * (prec ? 8 : 4));
   L.list = align_up(L.rec + nblocks * sizeof(BlkRec));
-  L.total = align_up(L.list + 4 * nblocks);
+  L.staging = align_up(L.list + 4 * nblocks);
+  L.total = align_up(L.staging + (uint64_t)kSlotBytes * nblocks);
   return L;
 }
 
@@ -104,6 +106,21 @@ void launch_encode(const EncParams& P, bool wide, cudaStream_t s) {
     else k_encode_wide<D, F64, false><<<grid, kThreads, 0, s>>>(P);
   }
   k_encode<D, F64><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
+  // K3: scan of the payload lengths, offset table, payload moves
+  CompactParams C;
+  C.sizes = P.status;
+  C.tstat = P.tstat;
+  C.nblocks = P.nblocks;
+  C.table0 = P.table0;
+  C.table = P.table;
+  C.table_base = P.table_base;
+  C.res = P.res;
+  C.staging = P.staging;
+  C.side = P.side;
+  C.rec = P.rec;
+  C.payload = P.payload;
+  k_scan_sizes<<<(unsigned)((P.nblocks + kScanTile - 1) / kScanTile), kScanThreads, 0, s>>>(C);
+  k_copy_payloads<<<(unsigned)((P.nblocks + kCopyWarps - 1) / kCopyWarps), 32 * kCopyWarps, 0, s>>>(C);
 }
 
 template <int D, bool F64>
@@ -148,6 +165,8 @@ EncParams make_enc(const void* const* axes, int dims, int prec, uint64_t count, 
   P.vec = vec ? 1 : 0;
   P.res = reinterpret_cast<DevResult*>(ws);
   P.status = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(ws) + L.status);
+  P.tstat = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(ws) + L.tstat);
+  P.staging = static_cast<uint8_t*>(ws) + L.staging;
   P.bounds = static_cast<uint8_t*>(ws) + L.bounds;
   P.rec = reinterpret_cast<BlkRec*>(static_cast<uint8_t*>(ws) + L.rec);
   P.wide_list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + L.list);
@@ -159,6 +178,18 @@ EncParams make_enc(const void* const* axes, int dims, int prec, uint64_t count, 
 extern "C" {
 
 const char* gpzb_version(void) { return "gpzb 0.1 sm_100a"; }
+
+#ifdef GPZB_DEBUG_STATS
+int gpzb_debug_counters(uint64_t* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, gpzb::g_dbg, 8 * sizeof(uint64_t));
+  if (reset) {
+    uint64_t z[8] = {0};
+    cudaMemcpyToSymbol(gpzb::g_dbg, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 const char* gpzb_reason_message(int r) {
   switch (r) {
@@ -237,7 +268,7 @@ int gpzb_decompress_workspace(const gpzb_header* h, uint64_t* ws_bytes) {
 
 int gpzb_workspace_reset_async(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t bs, void* stream) {
   const uint64_t nb = bs ? nblocks_of(count, bs) : 0;
-  const uint64_t need = align_up(sizeof(DevResult)) + 8 * nb;
+  const uint64_t need = enc_layout(nb, 1, 0).bounds;  // result record, sizes, scan tile words
   if (ws_bytes < std::min<uint64_t>(need, ws_bytes) || ws_bytes < align_up(sizeof(DevResult)))
     return GPZB_INVALID_ARGUMENT;
   return cuda_status(cudaMemsetAsync(ws, 0, std::min(need, ws_bytes), (cudaStream_t)stream));

@@ -67,6 +67,15 @@ __host__ __device__ inline unsigned long long err_code(uint64_t blk, int axis, i
   return ~((blk << 12) | ((uint64_t)(axis & 15) << 8) | (uint64_t)reason);
 }
 
+// Experiment builds (-DGPZB_DEBUG_STATS) count events here; read with
+// gpzb_debug_counters (declared only in the experiment tooling).
+#ifdef GPZB_DEBUG_STATS
+__device__ unsigned long long g_dbg[8];
+#define GPZB_DBG(i, v) atomicAdd(&g_dbg[i], (unsigned long long)(v))
+#else
+#define GPZB_DBG(i, v) ((void)0)
+#endif
+
 // ------------------------------------------------------ ordered encodings
 // u64 whose unsigned order equals the numeric order of the double.
 __device__ __forceinline__ unsigned long long ukey(double v) {
@@ -199,6 +208,22 @@ __device__ __forceinline__ void block_or(uint32_t (&v)[NV], uint32_t* ws /* kWar
     v[i] = r;
   }
   __syncthreads();
+}
+
+// The same with one RED per warp and value and a single barrier: `ws`
+// holds NV words that the caller zeroed before an earlier barrier and does
+// not touch again until a later one.
+template <int NV>
+__device__ __forceinline__ void block_or_z(uint32_t (&v)[NV], uint32_t* ws) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const uint32_t r = __reduce_or_sync(kFull, v[i]);
+    if (lane == 0 && r) red_or_shared(&ws[i], r);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = ws[i];
 }
 
 // ---------------------------------------------------------------- geometry

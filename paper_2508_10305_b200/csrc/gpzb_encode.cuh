@@ -31,7 +31,8 @@ struct EncParams {
   int vec;                 // all axis pointers 16B aligned
   DevResult* res;
   const void* bounds;      // K1 per-block [min,max] x dims in input precision
-  unsigned long long* status;  // look-back words, one per block
+  unsigned long long* status;  // payload length per block (K2) -> exclusive offset (K3)
+  unsigned long long* tstat;   // K3 scan tile look-back words
   uint8_t* payload;        // where block 0's payload starts
   uint8_t* table;          // where block 0's inclusive table entry goes (entry 1)
   uint8_t* table0;         // entry 0 (written by block 0) or null
@@ -43,6 +44,7 @@ struct EncParams {
   BlkRec* rec;             // per-block geometry records (K1.5)
   uint32_t* wide_list;     // blocks routed to the general encoder
   uint8_t* side;           // staging for the general encoder's payloads
+  uint8_t* staging;        // narrow payloads: one kSlotBytes slot per block (K3 concatenates)
 };
 
 // ----------------------------------------------------------------- loads
@@ -350,81 +352,5 @@ __device__ __forceinline__ void put_le(uint8_t* dst, uint64_t v, int nbytes) {
 }
 
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = kFlagAgg - 1;
-
-// Decoupled look-back by the whole CTA: each thread inspects one
-// predecessor per round (256 per round), the nearest inclusive prefix ends
-// the walk.  `ws` needs 2*kWarps + 2 words of shared scratch.
-__device__ __forceinline__ uint64_t lookback_cta(unsigned long long* status, uint64_t blk,
-                                                 unsigned long long* ws) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  uint64_t excl = 0;
-  long long look = (long long)blk - 1;
-  while (look >= 0) {
-    const long long idx = look - tid;
-    unsigned long long v = kFlagInc;
-    if (idx >= 0) {
-      do { v = ld_relaxed(&status[idx]); } while ((v >> 62) == 0);
-    }
-    // nearest predecessor (smallest tid) holding an inclusive prefix
-    const unsigned pm = __ballot_sync(kFull, (v >> 62) == 2);
-    if (lane == 0) ws[wid] = pm ? (unsigned long long)(wid * 32 + __ffs(pm) - 1) : ~0ull;
-    __syncthreads();
-    unsigned long long lim = ~0ull;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) lim = min(lim, ws[w]);
-    unsigned long long c = ((unsigned long long)tid <= lim) ? (v & kValMask) : 0ull;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
-    if (lane == 0) ws[kWarps + wid] = c;
-    __syncthreads();
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) excl += ws[kWarps + w];
-    __syncthreads();
-    if (lim != ~0ull) break;
-    look -= kThreads;
-  }
-  return excl;
-}
-
-// Copy `len` payload bytes held at byte 0.. of the u32 word array `src`
-// (shared or global, 16B aligned) to an arbitrary global address, as
-// 16-byte vector stores for the chunks the block owns outright and byte
-// stores for the two edge chunks shared with the neighbouring payloads.
-template <typename Src>
-__device__ __forceinline__ void realign_copy(uint8_t* dst, const Src* src, uint32_t len, int tid, int nthreads) {
-  const uint32_t al = (uint32_t)((uintptr_t)dst & 15);
-  uint8_t* g16 = dst - al;
-  const uint32_t nbytes = al + len;
-  const uint32_t nch = (nbytes + 15) >> 4;
-  const uint32_t nwords = (len + 3) >> 2;
-  const uint32_t sh = ((4 - (al & 3)) & 3) * 8;  // byte shift between source and destination words
-  for (uint32_t c = tid; c < nch; c += nthreads) {
-    uint32_t w[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      // destination bytes [16c + 4j, +4) hold payload bytes starting at s
-      const int s = (int)(16 * c + 4 * j) - (int)al;
-      const int wi = s >> 2;  // floor (s may be negative)
-      const uint32_t lo = (wi >= 0 && (uint32_t)wi < nwords) ? (uint32_t)src[wi] : 0u;
-      const uint32_t hi = (wi + 1 >= 0 && (uint32_t)(wi + 1) < nwords) ? (uint32_t)src[wi + 1] : 0u;
-      w[j] = sh ? __funnelshift_r(lo, hi, sh) : lo;
-    }
-    const uint32_t b0 = c * 16;
-    if (b0 >= al && b0 + 16 <= nbytes) {
-      __stcs(reinterpret_cast<uint4*>(g16 + b0), make_uint4(w[0], w[1], w[2], w[3]));
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t wb = b0 + 4 * j;
-        if (wb >= al && wb + 4 <= nbytes) {
-          *reinterpret_cast<uint32_t*>(g16 + wb) = w[j];
-        } else if (wb + 4 > al && wb < nbytes) {
-          for (int q = 0; q < 4; ++q)
-            if (wb + q >= al && wb + q < nbytes) g16[wb + q] = (uint8_t)(w[j] >> (8 * q));
-        }
-      }
-    }
-  }
-}
 
 }  // namespace gpzb

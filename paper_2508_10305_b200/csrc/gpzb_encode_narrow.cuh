@@ -1,36 +1,37 @@
-// K2: the 32-bit fast block encoder + container assembly.
+// K2: the 32-bit fast block encoder.
 //
-// One CTA (256 threads x 4 particles) per block, blocks taken in ticket
-// order for the decoupled look-back.  For "narrow" blocks (K1.5: every axis
-// on the certified-reciprocal quantizer, Π N <= 2^16, Σ log2 m <= 32, no
-// rank stream) it does the whole of pipeline._encode_block (pipeline.py:38-70):
+// One CTA (256 threads x 4 particles) per block, in launch order.  For
+// "narrow" blocks (K1.5: every axis on the certified-reciprocal quantizer,
+// Π N <= 2^16, Σ log2 m <= 32, no rank stream) it does the whole of
+// pipeline._encode_block (pipeline.py:38-70):
 //
 //   quantize (quantizer.py:142-191)  -> 32-bit (segment, offset) per particle
 //   pass A: presence bitmap over [0, Π N) -> distinct-segment ranks, run
 //           lengths and unique ids in one pass (RLE, codec.py:53-79)
-//   pass B: presence bitmap over (segment rank, offset) -> the stable
-//           (seg, off) order of blocksort.py:17-28 (ties are identical pairs)
-//   widths (codec.width_for) by OR-reduction, payload size, aggregate publish
-//   warp 0: decoupled look-back | warps 1-7: bit-pack header + streams
-//   all: realigned 16-byte vector stores of the payload + the table entry.
+//   widths (codec.width_for) by OR-reduction -> payload length
+//   offset order (blocksort.py:17-28): per-segment (offset, tie) masks, or a
+//           presence bitmap over (segment rank, offset), or in-group
+//           comparison ranks, or a stable 5-bit LSD (ties are identical
+//           pairs, so any tie order serialises to the same bytes)
+//   bit-pack header + streams into shared memory, then 16-byte stores of the
+//           payload into the block's staging slot and its length into
+//           sizes[blk] for the K3 scan + copy (gpzb_compact.cuh).
 //
-// Wide and error blocks only take part in the look-back and copy the
-// payload staged by K2w.
+// General blocks (staged by K2w) and error blocks only report their length.
 #pragma once
 
-#include "gpzb_encode.cuh"
+#include "gpzb_compact.cuh"
 
 namespace gpzb {
 
 #ifndef GPZB_K2_MINB
-#define GPZB_K2_MINB 7
+#define GPZB_K2_MINB 6
 #endif
 constexpr int kNarrowStageWords = 2048 + 32;  // narrow payload <= 7.7 KB
+constexpr uint32_t kGroupMaskWords = 3584;    // path 5: per-segment (offset, tie) masks
 
 struct NarrowSmem {
-  uint64_t blk;
-  uint64_t excl;
-  unsigned long long lb[2 * kWarps + 2];
+  BlkRec rec;  // this block's geometry record (K1.5), staged once
   uint32_t red[kWarps * 4];
   uint32_t scan32[kWarps];
   __align__(16) uint32_t cnt[kMaxBs];   // run length per distinct segment rank
@@ -40,6 +41,7 @@ struct NarrowSmem {
     struct { uint32_t bm[2048]; uint16_t wp[2048]; } a;
     struct { uint32_t bm[2048]; uint16_t wp[2048]; uint32_t cnt2[kMaxBs]; } b;
     struct { uint16_t segstart[kMaxBs]; uint32_t tmp[kMaxBs]; } c;
+    struct { uint32_t gm[kGroupMaskWords]; uint16_t segstart[kMaxBs]; } g;
     struct { uint32_t off[kMaxBs]; uint16_t sr[kMaxBs]; uint32_t bm[1024]; uint16_t wp[1024]; } l;
     uint32_t stage[kNarrowStageWords];
   };
@@ -50,10 +52,9 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// Global header (container.py:211-230) and table entry 0, by one thread of block 0.
+// Global header (container.py:211-230), by one thread of block 0.
 template <int D, bool F64>
 __device__ void write_global_header(const EncParams& P, double eb_abs) {
-  if (P.table0) put_le(P.table0, P.table_base, 8);
   if (!P.header) return;
   uint8_t* h = P.header;
   h[0] = 'G'; h[1] = 'P'; h[2] = 'Z'; h[3] = '1';
@@ -69,29 +70,47 @@ __device__ void write_global_header(const EncParams& P, double eb_abs) {
   put_le(h + 38, P.header_blocks, 8);
 }
 
-// Look-back by the whole CTA for a block of payload length L (aggregate
-// already published); publishes the inclusive prefix and the table entry.
-__device__ __forceinline__ uint64_t finish_lookback(const EncParams& P, uint64_t blk, uint64_t L,
-                                                    unsigned long long* ws) {
-#ifdef GPZB_NO_LOOKBACK  // experiment builds only: measures K2 without the scan (wrong container)
-  const uint64_t excl = (blk * 1600ull) % (64ull << 20);
-#else
-  const uint64_t excl = blk ? lookback_cta(P.status, blk, ws) : 0ull;
-#endif
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    if (blk > 0) st_relaxed(&P.status[blk], kFlagInc | (excl + L));
-    if (blk + 1 == P.nblocks) P.res->total_payload = excl + L;
+// Vectorised loads of a full block's 4 particles per thread (16-byte aligned axes).
+template <int D, typename T>
+__device__ __forceinline__ void load_full(const EncParams& P, uint64_t first, int p0, T (&x)[D][kItems]) {
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const T* base = reinterpret_cast<const T*>(P.axes[a]) + first + p0;
+    if constexpr (sizeof(T) == 4) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(base));
+      x[a][0] = v.x; x[a][1] = v.y; x[a][2] = v.z; x[a][3] = v.w;
+    } else {
+      const double2 v0 = __ldcs(reinterpret_cast<const double2*>(base));
+      const double2 v1 = __ldcs(reinterpret_cast<const double2*>(base) + 1);
+      x[a][0] = v0.x; x[a][1] = v0.y; x[a][2] = v1.x; x[a][3] = v1.y;
+    }
   }
-  if (tid < 8) P.table[blk * 8 + tid] = (uint8_t)((P.table_base + excl + L) >> (8 * tid));
-  return excl;
 }
 
-// The narrow-block work, specialised for full 1024-particle blocks (FULL:
-// no per-particle bounds predicates) and for the partial tail block.
+// Exact-division (segment, offset) of one particle: the rare fallback of the
+// certified quantizer, out of line so the fast path keeps no temporaries
+// alive for it.  Returns seg << 32 | off.
+template <int D, typename T>
+__device__ __noinline__ uint64_t redo_exact(T x0, T x1, T x2, const BlkRec* rec) {
+  uint32_t sk = 0, ok = 0, st = 1, sh = 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const T xa = a == 0 ? x0 : (a == 1 ? x1 : x2);
+    const double t = __dsub_rn((double)xa, rec->lo[a]);
+    const uint32_t q = (uint32_t)__double2ull_rz(__ddiv_rn(t, rec->w[a]));
+    const uint32_t b = rec->b[a];
+    sk += (q >> b) * st;
+    ok |= (q & ((1u << b) - 1u)) << (sh & 31);
+    st *= rec->N[a];
+    sh += b;
+  }
+  return ((uint64_t)sk << 32) | ok;
+}
+
 template <int D, bool F64, bool FULL>
 __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, const uint64_t blk,
-                                            const BlkRec* rec, const int n) {
+                                            const BlkRec* rec, const int n,
+                                            typename std::conditional<F64, double, float>::type (&x)[D][kItems]) {
   using T = typename std::conditional<F64, double, float>::type;
   constexpr int S = F64 ? 8 : 4;
   constexpr uint32_t H = 8 + D * (2 * S + 5) + 3;  // block header bytes (container.py:62-67)
@@ -101,24 +120,8 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
   const int p0 = tid * kItems;
 #define VALID(k) (FULL || p0 + (k) < n)
 
-  // ---- 1. load + quantize to 32-bit (segment, offset)
-  T x[D][kItems];
-  if constexpr (FULL) {
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      const T* base = reinterpret_cast<const T*>(P.axes[a]) + first + p0;
-      if constexpr (sizeof(T) == 4) {
-        const float4 v = __ldcs(reinterpret_cast<const float4*>(base));
-        x[a][0] = v.x; x[a][1] = v.y; x[a][2] = v.z; x[a][3] = v.w;
-      } else {
-        const double2 v0 = __ldcs(reinterpret_cast<const double2*>(base));
-        const double2 v1 = __ldcs(reinterpret_cast<const double2*>(base) + 1);
-        x[a][0] = v0.x; x[a][1] = v0.y; x[a][2] = v1.x; x[a][3] = v1.y;
-      }
-    }
-  } else {
-    load_particles<D, T>(P, first, n, p0, x);
-  }
+  // ---- 1. load (full blocks: already issued by the caller) + quantize to 32-bit (segment, offset)
+  if constexpr (!FULL) load_particles<D, T>(P, first, n, p0, x);
   const uint32_t PN = rec->PN, sumb = rec->sumb;
   uint32_t seg[kItems], off[kItems];
 #pragma unroll
@@ -153,18 +156,10 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
 #pragma unroll
       for (int k = 0; k < kItems; ++k) {
         if (!(redo & (1u << k))) continue;
-        uint32_t sk = 0, ok = 0, st = 1, sh = 0;
-        for (int a = 0; a < D; ++a) {
-          const double t = __dsub_rn((double)x[a][k], rec->lo[a]);
-          const uint32_t q = exact_floor_div(t, rec->w[a]);
-          const uint32_t b = rec->b[a];
-          sk += (q >> b) * st;
-          ok |= (q & ((1u << b) - 1u)) << (sh & 31);
-          st *= rec->N[a];
-          sh += b;
-        }
-        seg[k] = sk;
-        off[k] = ok;
+        const uint64_t so = redo_exact<D, T>(x[0][k], D > 1 ? x[D > 1 ? 1 : 0][k] : T(0),
+                                             D > 2 ? x[D > 2 ? 2 : 0][k] : T(0), rec);
+        seg[k] = (uint32_t)(so >> 32);
+        off[k] = (uint32_t)so;
       }
     }
   }
@@ -177,6 +172,7 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
   bm_zero(sm.u.a.bm, nwA);
   reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(0, 0, 0, 0);
   if (tid == 0) sm.uniqp[0] = 0;
+  if (tid < 3) sm.red[tid] = 0;  // block_or_z accumulators
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < kItems; ++k)
@@ -210,17 +206,52 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
     }
   }
   uint32_t red[3] = {off_or, c_or, d_or};
-  block_or<3>(red, sm.red);
+  block_or_z<3>(red, sm.red);
   const uint32_t w_off = bitlen32(red[0]), w_cnt = bitlen32(red[1]), w_del = bitlen32(red[2]);
   const uint32_t Ld = (U * w_del + 7) >> 3, Lc = (U * w_cnt + 7) >> 3, Lo = ((uint32_t)n * w_off + 7) >> 3;
   const uint32_t L = H + Ld + Lc + Lo;
-  if (tid == 0) st_relaxed(&P.status[blk], (blk == 0 ? kFlagInc : kFlagAgg) | L);
+  if (tid == 0) P.status[blk] = L;  // payload length for the K3 scan
 
   // ---- 4. order the offsets: (segment rank, offset) composite ranks
   int path = 0;
   if (w_off) {
     uint32_t pos[kItems];
-    if (w_cnt > 3 && sumb <= 16 && (U << sumb) <= 65536u) {
+    // (offset, tie) codes are unique inside a segment group, so a per-group
+    // presence mask ranks them directly; ties are identical (seg, off)
+    // pairs, any order of which serialises to the same bytes
+    const uint32_t cb = sumb + w_cnt;  // tie < max run length < 2^w_cnt
+    const uint32_t W = cb <= 5 ? 1u : (1u << (cb - 5));
+    if (cb <= 8 && U * W <= kGroupMaskWords) {
+      path = 5;
+      uint32_t* gm = sm.u.g.gm;
+      for (uint32_t w = tid; w < (U * W + 3) >> 2; w += kThreads)
+        reinterpret_cast<uint4*>(gm)[w] = make_uint4(0, 0, 0, 0);
+      uint32_t tot;
+      uint32_t ex = block_excl_scan<uint32_t>(csum, tot, sm.scan32);  // its barriers order the zeroing
+#pragma unroll
+      for (int j = 0; j < kItems; ++j) {
+        if (p0 + j < (int)U) sm.u.g.segstart[p0 + j] = (uint16_t)ex;
+        ex += cloc[j];
+      }
+      uint32_t code[kItems];
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        code[k] = (off[k] << w_cnt) | tie[k];
+        if VALID(k) red_or_shared(&gm[srank[k] * W + (code[k] >> 5)], 1u << (code[k] & 31));
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        pos[k] = 0;
+        if VALID(k) {
+          const uint32_t* g = gm + srank[k] * W;
+          const uint32_t wi = code[k] >> 5;
+          uint32_t r = __popc(g[wi] & ((1u << (code[k] & 31)) - 1u));
+          for (uint32_t i = 0; i < wi; ++i) r += __popc(g[i]);
+          pos[k] = sm.u.g.segstart[srank[k]] + r;
+        }
+      }
+    } else if (w_cnt > 3 && sumb <= 16 && (U << sumb) <= 65536u) {
       path = 1;
       const int nw = (int)(((U << sumb) + 31) >> 5);
       bm_zero(sm.u.b.bm, nw);
@@ -326,14 +357,14 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
   }
   __syncthreads();  // soff complete; union free for the stage
 
-  // ---- 5. bit-pack into the stage (payload byte 0 = stage byte 0); the offset is not needed yet
+  // ---- 5. bit-pack header + streams into the stage (payload byte 0 = stage byte 0)
   uint32_t* st = sm.u.stage;
   if (tid == 0) atomicAdd(&R->path_blocks[path], 1ull);
+  const uint32_t nquads = (L + 15) >> 4;
+  for (uint32_t w = tid; w < nquads; w += kThreads) reinterpret_cast<uint4*>(st)[w] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
   {
     const int t = tid, nt = kThreads;
-    const uint32_t nquads = (L + 15) >> 4;
-    for (uint32_t w = t; w < nquads; w += nt) reinterpret_cast<uint4*>(st)[w] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
     if (t < 32) {
       // block header fields, one per lane (container.serialize_block, container.py:107-121)
       const int f = t;
@@ -394,9 +425,9 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
   }
   __syncthreads();
 
-  // ---- 6. decoupled look-back (whole CTA), then realigned vector stores
-  const uint64_t excl = finish_lookback(P, blk, L, sm.lb);
-  realign_copy(P.payload + excl, st, L, tid, kThreads);
+  // ---- 6. the stage to this block's 16-byte aligned staging slot (K3 moves it into place)
+  uint4* slot = reinterpret_cast<uint4*>(P.staging + blk * (uint64_t)kSlotBytes);
+  for (uint32_t w = tid; w < nquads; w += kThreads) __stcg(slot + w, reinterpret_cast<const uint4*>(st)[w]);
 #undef VALID
 }
 
@@ -406,27 +437,29 @@ __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncPara
   const int tid = threadIdx.x;
   DevResult* R = P.res;
 
-  if (tid == 0) sm.blk = atomicAdd(&R->ticket, 1ull);
+  // Blocks in launch order (CTAs are dispatched in blockIdx order, which is
+  // what the look-back's forward progress needs; no ticket atomic).
+  using T = typename std::conditional<F64, double, float>::type;
+  const uint64_t blk = blockIdx.x;
+  const uint64_t first = blk * (uint64_t)P.bs;
+  const int n = (int)min((uint64_t)P.bs, P.count - first);
+  const bool full = n == kMaxBs && P.vec;
+  T x[D][kItems];
+  if (full) load_full<D, T>(P, first, tid * kItems, x);  // in flight while the record is staged
+  if (tid < 8) reinterpret_cast<uint4*>(&sm.rec)[tid] = reinterpret_cast<const uint4*>(P.rec + blk)[tid];
   __syncthreads();
-  const uint64_t blk = sm.blk;
-  const BlkRec* rec = P.rec + blk;
+  const BlkRec* rec = &sm.rec;
   const uint32_t kind = rec->kind;
   if (blk == 0 && tid == 32) write_global_header<D, F64>(P, R->eb_abs);
 
   if (kind != KIND_NARROW) {
-    // wide (staged by K2w) or error block (size 0): look-back + copy only
-    const uint64_t L = (kind == KIND_WIDE) ? rec->side_len : 0ull;
-    if (tid == 0) st_relaxed(&P.status[blk], (blk == 0 ? kFlagInc : kFlagAgg) | L);
-    const uint64_t ex = finish_lookback(P, blk, L, sm.lb);
-    if (L) realign_copy(P.payload + ex, reinterpret_cast<const uint32_t*>(P.side + rec->side_off),
-                        (uint32_t)L, tid, kThreads);
+    // general blocks were staged by K2w; error blocks contribute no bytes
+    if (tid == 0) P.status[blk] = (kind == KIND_WIDE) ? rec->side_len : 0ull;
     return;
   }
 
-  const uint64_t first = blk * (uint64_t)P.bs;
-  const int n = (int)min((uint64_t)P.bs, P.count - first);
-  if (n == kMaxBs && P.vec) narrow_body<D, F64, true>(P, sm, blk, rec, n);
-  else narrow_body<D, F64, false>(P, sm, blk, rec, n);
+  if (full) narrow_body<D, F64, true>(P, sm, blk, rec, n, x);
+  else narrow_body<D, F64, false>(P, sm, blk, rec, n, x);
 }
 
 }  // namespace gpzb

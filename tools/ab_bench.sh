@@ -9,7 +9,8 @@ import json,sys
 for l in sys.stdin:
     try: d=json.loads(l)
     except Exception: print(l.strip()); continue
-    print('comp %.1f decomp %.1f k_encode %.3f k_decode %.3f k_range %.3f cr %.3f clk %s' % (d['value'], d['decompress']['value'], d['kernels']['k_encode_ms'], d['kernels']['k_decode_ms'], d['kernels']['k_range_ms'], d['compression_ratio'], d['clocks']))
+    pd=d['kernels']['per_dataset_ms']; f=lambda v: '/'.join('%.3f' % x if x else '-' for x in v)
+    print('comp %.1f decomp %.1f k_encode %s k_decode %s k_range %.3f cr %.3f clk %s' % (d['value'], d['decompress']['value'], f(pd['k_encode']), f(pd['k_decode']), d['kernels']['k_range_ms'], d['compression_ratio'], d['clocks']['sm_mhz'] if d['clocks'] else None))
 " >> gpurun_out/ab.txt
 done
 cat gpurun_out/ab.txt
