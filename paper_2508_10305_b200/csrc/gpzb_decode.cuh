@@ -226,10 +226,10 @@ struct DecSmem {
   unsigned long long scan[2 * kWarps];
   uint32_t red[kWarps];
   uint32_t seen[kMaxBs / 32];
+  uint32_t rstart[kMaxBs / 32];  // fast path: bit p set <=> a run starts at position p
   __align__(16) uint32_t words[kDecStageWords];
   __align__(16) uint64_t uniq[kMaxBs];
   __align__(16) uint32_t starts[kMaxBs];
-  __align__(16) uint16_t runidx[kMaxBs];
 };
 
 __device__ __forceinline__ uint32_t get_bits32(const uint32_t* st, uint32_t pos, uint32_t nbits) {
@@ -268,7 +268,7 @@ __device__ __forceinline__ void block_excl_scan2(unsigned long long& a, unsigned
 }
 
 #ifndef GPZB_K4_MINB
-#define GPZB_K4_MINB 5
+#define GPZB_K4_MINB 6
 #endif
 
 // Load the payload window into shared memory (16B chunks; edges bytewise).
@@ -328,6 +328,7 @@ __device__ __forceinline__ void decode_fast(const DecParams& P, DecSmem& sm, con
   const uint32_t al = (uint32_t)((uintptr_t)pay & 15);
   const uint32_t plen = so + ((kMaxBs * wo + 7) >> 3);
   load_window(P, sm, pay, al, plen);
+  if (tid < kMaxBs / 32) sm.rstart[tid] = 0;
   __syncthreads();
   const uint8_t* pb = reinterpret_cast<const uint8_t*>(sm.words) + al;
   const uint32_t pbit = 8 * al;
@@ -370,7 +371,7 @@ __device__ __forceinline__ void decode_fast(const DecParams& P, DecSmem& sm, con
         if (cn[j] < 1) fl |= 1u << 4;             // pipeline.py:118-119
         if (u >= rec->PN) fl |= 1u << 13;         // quantizer.py:262-263
         sm.uniq[r] = u;
-        sm.starts[r] = cex;
+        if (cex < (uint32_t)kMaxBs) red_or_shared(&sm.rstart[cex >> 5], 1u << (cex & 31));
         cex += cn[j];
         prev = u;
       }
@@ -391,17 +392,28 @@ __device__ __forceinline__ void decode_fast(const DecParams& P, DecSmem& sm, con
     if (tid == 0) report_decode_error(R, blk, v[0]);
     return;
   }
-  // run index of every position: each run writes its own span (counts are
-  // validated: >= 1, summing to 1024)
+  // run index of every position = (run starts at or before it) - 1: a rank
+  // in the 1024-bit run-start map (counts are validated: >= 1, summing to
+  // 1024, so the starts are distinct and in range)
+  uint32_t run[kItems];
+  {
+    const int lane = tid & 31;
+    const uint32_t c = __popc(sm.rstart[lane]);
+    uint32_t incl = c;
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const uint32_t r = p0 + j;
-    if (r < U) {
-      const uint32_t s0 = sm.starts[r], s1 = (r + 1 < U) ? sm.starts[r + 1] : (uint32_t)kMaxBs;
-      for (uint32_t p = s0; p < s1; ++p) sm.runidx[p] = (uint16_t)r;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int wsel = p0 >> 5;  // this thread's 4 positions share one map word
+    const uint32_t base = __shfl_sync(kFull, incl - c, wsel);
+    const uint32_t word = sm.rstart[wsel];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const uint32_t b = (uint32_t)(p0 + k) & 31;
+      run[k] = base + __popc(word & (0xffffffffu >> (31 - b))) - 1;
     }
   }
-  __syncthreads();
   double lo[D], w[D];
   uint32_t bsh[D], shifts[D], Nn[D], mgm[D], mgl[D];
   {
@@ -418,8 +430,6 @@ __device__ __forceinline__ void decode_fast(const DecParams& P, DecSmem& sm, con
       mgl[a] = rec->mg_l[a];
     }
   }
-  const uint2 ri = *reinterpret_cast<const uint2*>(&sm.runidx[p0]);
-  const uint32_t run[kItems] = {ri.x & 0xffffu, ri.x >> 16, ri.y & 0xffffu, ri.y >> 16};
   T vals[D][kItems];
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {

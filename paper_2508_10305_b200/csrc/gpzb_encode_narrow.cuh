@@ -221,7 +221,7 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
     // pairs, any order of which serialises to the same bytes
     const uint32_t cb = sumb + w_cnt;  // tie < max run length < 2^w_cnt
     const uint32_t W = cb <= 5 ? 1u : (1u << (cb - 5));
-    if (cb <= 8 && U * W <= kGroupMaskWords) {
+    if (cb <= 7 && U * W <= kGroupMaskWords) {
       path = 5;
       uint32_t* gm = sm.u.g.gm;
       for (uint32_t w = tid; w < (U * W + 3) >> 2; w += kThreads)
@@ -244,10 +244,21 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
       for (int k = 0; k < kItems; ++k) {
         pos[k] = 0;
         if VALID(k) {
-          const uint32_t* g = gm + srank[k] * W;
-          const uint32_t wi = code[k] >> 5;
-          uint32_t r = __popc(g[wi] & ((1u << (code[k] & 31)) - 1u));
-          for (uint32_t i = 0; i < wi; ++i) r += __popc(g[i]);
+          // codes below mine in the group's 32 / 64 / 128-bit mask (W is block-uniform)
+          const uint32_t c = code[k];
+          uint32_t r;
+          if (W == 1) {
+            r = __popc(gm[srank[k]] & ((1u << c) - 1u));
+          } else if (W == 2) {
+            const uint2 m = reinterpret_cast<const uint2*>(gm)[srank[k]];
+            r = __popcll((((uint64_t)m.y << 32) | m.x) & ((1ull << c) - 1ull));
+          } else {
+            const uint4 m = reinterpret_cast<const uint4*>(gm)[srank[k]];
+            const uint64_t lo = ((uint64_t)m.y << 32) | m.x, hi = ((uint64_t)m.w << 32) | m.z;
+            const uint32_t ch = c & 63;
+            r = c < 64 ? __popcll(lo & ((1ull << ch) - 1ull))
+                       : __popcll(lo) + __popcll(hi & ((1ull << ch) - 1ull));
+          }
           pos[k] = sm.u.g.segstart[srank[k]] + r;
         }
       }
