@@ -45,8 +45,9 @@ struct __align__(16) DecRec {
   uint8_t chk_mask;   // bit a: reconstruction may be non-finite -> per-element check
   uint8_t pn_big;     // Π N > 2^32 (64-bit delinearisation)
   uint8_t pn_all;     // Π N >= 2^64 (every id in range)
-  uint8_t fast_body;  // 32-bit decode body applies (see k_decode)
-  uint8_t pad[6];
+  uint8_t fast_body;  // 32-bit decode body applies (see k_decode); 2: with the midpoint table
+  uint16_t lut1, lut2;  // fast_body 2: table offsets of axes 1 and 2 (axis 0 starts at 0)
+  uint16_t lut_n;       // fast_body 2: table entries (Σ N_a 2^b_a)
 };
 static_assert(sizeof(DecRec) == 128, "DecRec layout");
 
@@ -65,6 +66,10 @@ struct DecParams {
 };
 
 constexpr int kDecStageWords = 5120;  // 20 KB payload window (legit blocks <= 19.2 KB)
+#ifndef GPZB_LUT_UMAX
+#define GPZB_LUT_UMAX 512
+#endif
+constexpr int kLutEntries = 4096;     // midpoint table (f32 entries) in the window after unpacking
 
 __device__ __forceinline__ uint64_t ld_le(const uint8_t* p, int nbytes) {
   uint64_t v = 0;
@@ -218,6 +223,21 @@ __global__ void __launch_bounds__(256) k_decode_plan(const DecParams P) {
   rec.fast_body = (n == (uint32_t)kMaxBs && !PRES && w4[0] <= 32 && w4[1] <= 32 && w4[2] <= 32 && sumb <= 32 &&
                    !rec.pn_big && rec.fast_mask == (1u << D) - 1 && rec.chk_mask == 0 && rec.geo_bits == 0)
                       ? 1 : 0;
+  if (rec.fast_body) {
+    // every reconstructable value of the block, one table entry per bin
+    // (q in [0, N_a 2^b_a) per axis), when the table fits the stage
+    uint64_t tot = 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      if (a == 1) rec.lut1 = (uint16_t)tot;
+      if (a == 2) rec.lut2 = (uint16_t)tot;
+      tot += (uint64_t)rec.N[a] << rec.b[a];
+    }
+    if (tot <= (uint64_t)kLutEntries / (F64 ? 2 : 1) && U <= GPZB_LUT_UMAX) {
+      rec.fast_body = 2;
+      rec.lut_n = (uint16_t)tot;
+    }
+  }
   P.rec[blk] = rec;
 }
 
@@ -357,6 +377,7 @@ __device__ __forceinline__ void decode_fast(const DecParams& P, DecSmem& sm, con
   uint32_t off[kItems];
 #pragma unroll
   for (int k = 0; k < kItems; ++k) off[k] = get_bits32(sm.words, pbit + 8 * so + (p0 + k) * wo, wo);
+  const bool lut = rec->fast_body == 2;
   unsigned long long dtot, ctot;
   block_excl_scan2(dsum, csum, dtot, ctot, sm.scan);
   {
@@ -414,6 +435,57 @@ __device__ __forceinline__ void decode_fast(const DecParams& P, DecSmem& sm, con
       run[k] = base + __popc(word & (0xffffffffu >> (31 - b))) - 1;
     }
   }
+  T vals[D][kItems];
+  if (lut) {
+    // midpoint table over the (now consumed) payload window, then one lookup per coordinate
+    T* tab = reinterpret_cast<T*>(sm.words);
+    const uint32_t nt = rec->lut_n, l1 = rec->lut1, l2 = rec->lut2;
+    for (uint32_t i = tid; i < nt; i += kThreads) {
+      const int a = (D > 2 && i >= l2) ? 2 : (D > 1 && i >= l1) ? 1 : 0;
+      const uint32_t q = i - (a == 0 ? 0u : a == 1 ? l1 : l2);
+      const double h = __longlong_as_double((long long)(0x4320000000000000ull + 2 * (uint64_t)q + 1));
+      const double aq = __dsub_rn(h, 2251799813685248.0);
+      tab[i] = (T)__dadd_rn(rec->lo[a], __dmul_rn(aq, rec->w[a]));
+    }
+    // each run's table bases (bin seg_a << b_a per axis, 16 bits per axis),
+    // spread over all threads (U may be far below the thread count)
+    for (uint32_t r = tid; r < U; r += kThreads) {
+      uint32_t rest = (uint32_t)sm.uniq[r];
+      uint64_t pk = 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        uint32_t sa;
+        if (a + 1 < D) {
+          const uint32_t qd = magic_div(rest, rec->mg_m[a], rec->mg_l[a]);
+          sa = rest - qd * rec->N[a];
+          rest = qd;
+        } else {
+          sa = rest;
+        }
+        const uint32_t base = (a == 0 ? 0u : a == 1 ? l1 : l2) + (sa << rec->b[a]);
+        pk |= (uint64_t)(base & 0xffffu) << (16 * a);
+      }
+      sm.uniq[r] = pk;
+    }
+    __syncthreads();
+    uint32_t shifts[D], masks[D];
+    {
+      uint32_t sft = 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        shifts[a] = sft;
+        masks[a] = (1u << rec->b[a]) - 1u;
+        sft += rec->b[a];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const uint64_t pk = sm.uniq[run[k]];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+        vals[a][k] = tab[((uint32_t)(pk >> (16 * a)) & 0xffffu) + ((off[k] >> shifts[a]) & masks[a])];
+    }
+  } else {
   double lo[D], w[D];
   uint32_t bsh[D], shifts[D], Nn[D], mgm[D], mgl[D];
   {
@@ -430,7 +502,6 @@ __device__ __forceinline__ void decode_fast(const DecParams& P, DecSmem& sm, con
       mgl[a] = rec->mg_l[a];
     }
   }
-  T vals[D][kItems];
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
     uint32_t rest = (uint32_t)sm.uniq[run[k]];
@@ -451,6 +522,7 @@ __device__ __forceinline__ void decode_fast(const DecParams& P, DecSmem& sm, con
       const double aq = __dsub_rn(h, 2251799813685248.0);
       vals[a][k] = (T)__dadd_rn(lo[a], __dmul_rn(aq, w[a]));
     }
+  }
   }
   const uint64_t idx0 = (P.out_offsets ? P.out_offsets[blk] : blk * (uint64_t)P.bs) + p0;
 #pragma unroll
