@@ -13,6 +13,8 @@
  *   gpzb_parse_header    <- container.read_container     container.py:245-267
  *   gpzb_decompress      <- pipeline.decompress          pipeline.py:160-205
  *   gpzb_block_counts    <- (iter_decompressed_blocks support, pipeline.py:208-215)
+ *   gpzb_pair_blocks     <- metrics.pair_blocks          metrics.py:49-81
+ *   gpzb_pair_stats      <- metrics.nrmse / verify_bound metrics.py:84-152
  *
  * Conventions
  *  - Every device pointer is caller-owned (PyTorch's caching allocator in the
@@ -182,6 +184,34 @@ int gpzb_decompress_result(void* ws, uint64_t ws_bytes, const gpzb_header* h, vo
 int gpzb_decompress(const uint8_t* container, uint64_t container_len, const gpzb_header* h,
                     void* const* axes_out, uint64_t out_capacity, const uint64_t* out_offsets,
                     void* ws, uint64_t ws_bytes, void* stream, gpzb_result* res);
+
+/* ---- error-bound verification (K5) --------------------------------------- */
+
+/* Device workspace of gpzb_pair_blocks / gpzb_pair_stats for `count` pairs. */
+int gpzb_pair_workspace(uint64_t count, int dims, uint64_t* ws_bytes);
+
+/* metrics.pair_blocks (metrics.py:54-81): per block, quantize the original
+ * and the reconstruction (cast to the original's precision) with the
+ * original block's geometry, sort each by (seg_id, offset, index) and write
+ * the positional pairing as global indices into orig_idx / rec_idx (int64,
+ * `count` each).  Synchronous; errors as in compression (non-finite axis:
+ * DomainError with the axis, original first; geometry: WidthOverflow with
+ * the first failing block). */
+int gpzb_pair_blocks(const void* const* orig, const void* const* rec, int dims, int precision,
+                     int rec_precision, uint64_t count, double eb_abs, uint32_t block_size,
+                     uint32_t target_segs_per_axis, int64_t* orig_idx, int64_t* rec_idx, void* ws,
+                     uint64_t ws_bytes, void* stream, gpzb_result* res);
+
+/* metrics.nrmse / verify_bound statistics over paired values (null index
+ * arrays: identity pairing).  stats[0] = max |o - r|; per axis a:
+ * stats[1 + 3a] = Σ (o - r)^2, stats[2 + 3a] = min o, stats[3 + 3a] = max o
+ * (all in float64, reduced in a fixed order).  Pairs with |o - r| > eb_abs
+ * are written to viol (up to viol_cap triples: axis << 56 | pair position,
+ * original index, |error| bits) and counted in viol_count.  Synchronous. */
+int gpzb_pair_stats(const void* const* orig, const void* const* rec, int dims, int precision,
+                    int rec_precision, uint64_t count, const int64_t* orig_idx, const int64_t* rec_idx,
+                    double eb_abs, uint64_t* viol, uint64_t viol_cap, void* ws, uint64_t ws_bytes,
+                    void* stream, double* stats, uint64_t* viol_count);
 
 /* ---- diagnostics -------------------------------------------------------- */
 

@@ -18,6 +18,8 @@ algorithm" is exactly its float64 arithmetic and its byte format:
 * stage 4 compact   — ``container.py:102-303`` (block header, prefix-sum
   offset table, 46-byte global header)
 * orchestration     — ``pipeline.py:38-215``
+* evaluation        — ``metrics.py:49-152`` (block pairing, NRMSE, PSNR,
+  bound check: the checker for the GPU K5 kernels)
 
 Parity is PINNED: ``tests/golden/`` holds containers, reconstructions and
 error outcomes produced by the reference itself (``tests/golden/make_golden.py``
@@ -527,6 +529,76 @@ def iter_blocks(data: bytes):
             yield decode_block(payload[int(table[i]):int(table[i + 1])], h)
         except OracleError as exc:
             raise CorruptData(f"block {i}: {exc}") from None
+
+
+# --------------------------------------------------------------------------
+# evaluation — block pairing, NRMSE, PSNR, bound check (metrics.py:49-200)
+
+
+def block_order(block_axes, g: Geometry, eb_abs: float, prec: int) -> np.ndarray:
+    """metrics._block_order, metrics.py:49-51: lexsort by (seg, offset, index)."""
+    qs = [quantize_axis(a, g.mins[i], g.maxs[i], g.Q[i], eb_abs, prec) for i, a in enumerate(block_axes)]
+    seg, off = linearize(qs, g)
+    return np.lexsort((np.arange(seg.size), off, seg))
+
+
+def pair_blocks(orig, rec, block_size: int, target: int, eb_abs: float):
+    """metrics.pair_blocks, metrics.py:54-81 (eb_abs already resolved)."""
+    orig, prec = check_axes(orig)
+    rec = [np.asarray(a) for a in rec]
+    if len(orig) != len(rec) or orig[0].size != rec[0].size:
+        raise DomainError("datasets differ in shape, cannot pair")
+    check_axes(rec)
+    n = orig[0].size
+    oi = np.empty(n, np.int64)
+    ri = np.empty(n, np.int64)
+    for start in range(0, n, block_size):
+        sl = slice(start, min(start + block_size, n))
+        ob = [a[sl] for a in orig]
+        rb = [a[sl].astype(_NPTYPE[prec]) for a in rec]
+        g = geometry([float(a.min()) for a in ob], [float(a.max()) for a in ob], eb_abs, target, prec)
+        oi[sl] = start + block_order(ob, g, eb_abs, prec)
+        ri[sl] = start + block_order(rb, g, eb_abs, prec)
+    return oi, ri
+
+
+def nrmse(o, r, pairing=None) -> float:
+    """metrics.nrmse, metrics.py:84-104."""
+    o = np.asarray(o, dtype=np.float64)
+    r = np.asarray(r, dtype=np.float64)
+    if pairing is not None:
+        o = o[pairing[0]]
+        r = r[pairing[1]]
+    if o.size == 0:
+        return 0.0
+    rmse = math.sqrt(float(np.mean((o - r) ** 2)))
+    span = float(o.max() - o.min())
+    if span <= 0.0:
+        if rmse == 0.0:
+            return 0.0
+        raise DomainError("degenerate field range with nonzero error")
+    return rmse / span
+
+
+def aggregate_psnr(values) -> float:
+    """metrics.aggregate_psnr, metrics.py:107-119."""
+    values = [float(v) for v in values]
+    if not values:
+        raise DomainError("aggregate PSNR of no fields")
+    mean_sq = sum(v * v for v in values) / len(values)
+    return math.inf if mean_sq == 0.0 else -20.0 * math.log10(math.sqrt(mean_sq))
+
+
+def verify_bound(orig, rec, eb_abs: float, block_size: int, target: int):
+    """metrics.verify_bound, metrics.py:131-152 -> (max_err, violations, checked)."""
+    oi, ri = pair_blocks(orig, rec, block_size, target, eb_abs)
+    max_err, viol = 0.0, []
+    for a in range(len(orig)):
+        d = np.abs(np.asarray(orig[a], np.float64)[oi] - np.asarray(rec[a], np.float64)[ri])
+        if d.size:
+            max_err = max(max_err, float(d.max()))
+        viol.extend((a, int(oi[i]), float(d[i])) for i in np.flatnonzero(d > eb_abs))
+    return max_err, viol, orig[0].size * len(orig)
 
 
 # --------------------------------------------------------------------------

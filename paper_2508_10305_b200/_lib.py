@@ -78,6 +78,11 @@ SIGNATURES = {
     "gpzb_decompress": (_I32, [_VP, _U64, _HDR, ctypes.POINTER(_VP), _U64, _VP, _VP, _U64, _VP, _RES]),
     "gpzb_decompress_async": (_I32, [_VP, _U64, _HDR, ctypes.POINTER(_VP), _U64, _VP, _VP, _U64, _VP]),
     "gpzb_decompress_result": (_I32, [_VP, _U64, _HDR, _VP, _RES]),
+    "gpzb_pair_workspace": (_I32, [_U64, _I32, ctypes.POINTER(_U64)]),
+    "gpzb_pair_blocks": (_I32, [ctypes.POINTER(_VP), ctypes.POINTER(_VP), _I32, _I32, _I32, _U64, _D, _U32, _U32,
+                                _VP, _VP, _VP, _U64, _VP, _RES]),
+    "gpzb_pair_stats": (_I32, [ctypes.POINTER(_VP), ctypes.POINTER(_VP), _I32, _I32, _I32, _U64, _VP, _VP, _D,
+                               _VP, _U64, _VP, _U64, _VP, ctypes.POINTER(_D), ctypes.POINTER(_U64)]),
     "gpzb_reason_message": (ctypes.c_char_p, [_I32]),
     "gpzb_version": (ctypes.c_char_p, []),
 }

@@ -11,6 +11,7 @@
 #include "gpzb_encode.cuh"
 #include "gpzb_encode_narrow.cuh"
 #include "gpzb_encode_wide.cuh"
+#include "gpzb_metrics.cuh"
 
 using namespace gpzb;
 
@@ -147,6 +148,36 @@ void launch_decode(const DecParams& P, bool pres, cudaStream_t s) {
       else FN<3, false>(__VA_ARGS__);                        \
     }                                                        \
   } while (0)
+
+template <int D, bool F64, bool R64>
+void launch_pair_blocks(const PairParams& P, cudaStream_t s) {
+  using T = typename std::conditional<F64, double, float>::type;
+  using R = typename std::conditional<R64, double, float>::type;
+  k_pair_blocks<D, T, R><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
+}
+
+template <int D, bool F64, bool R64>
+void launch_pair_stats(const PairParams& P, unsigned grid, cudaStream_t s) {
+  using T = typename std::conditional<F64, double, float>::type;
+  using R = typename std::conditional<R64, double, float>::type;
+  k_pair_stats<D, T, R><<<grid, kThreads, 0, s>>>(P);
+  k_pair_stats_final<D><<<1, 32, 0, s>>>(P, (int)grid);
+}
+
+#define DISPATCH_DPR(dims, prec, rprec, FN, ...)                                   \
+  do {                                                                             \
+    if (prec) {                                                                    \
+      if (rprec) { if (dims == 1) FN<1, true, true>(__VA_ARGS__); else if (dims == 2) FN<2, true, true>(__VA_ARGS__); else FN<3, true, true>(__VA_ARGS__); } \
+      else { if (dims == 1) FN<1, true, false>(__VA_ARGS__); else if (dims == 2) FN<2, true, false>(__VA_ARGS__); else FN<3, true, false>(__VA_ARGS__); } \
+    } else {                                                                       \
+      if (rprec) { if (dims == 1) FN<1, false, true>(__VA_ARGS__); else if (dims == 2) FN<2, false, true>(__VA_ARGS__); else FN<3, false, true>(__VA_ARGS__); } \
+      else { if (dims == 1) FN<1, false, false>(__VA_ARGS__); else if (dims == 2) FN<2, false, false>(__VA_ARGS__); else FN<3, false, false>(__VA_ARGS__); } \
+    }                                                                              \
+  } while (0)
+
+unsigned pair_stats_grid(uint64_t count) {
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((count + kThreads - 1) / kThreads, (uint64_t)sm_count() * 8));
+}
 
 EncParams make_enc(const void* const* axes, int dims, int prec, uint64_t count, uint32_t bs,
                    void* ws) {
@@ -551,6 +582,96 @@ int gpzb_decompress(const uint8_t* c, uint64_t len, const gpzb_header* h, void* 
   int st = gpzb_decompress_async(c, len, h, axes_out, out_cap, out_offsets, ws, ws_bytes, stream);
   if (st) return res->status = st;
   return gpzb_decompress_result(ws, ws_bytes, h, stream, res);
+}
+
+
+/* ---- K5: pairing and error-bound statistics (metrics.py:49-152) ---- */
+
+int gpzb_pair_workspace(uint64_t count, int dims, uint64_t* ws_bytes) {
+  if (dims < 1 || dims > 3) return GPZB_INVALID_ARGUMENT;
+  const uint64_t ns = 1 + 3 * (uint64_t)dims;
+  *ws_bytes = align_up(sizeof(DevResult)) + align_up(8 + 8 * ns) + align_up(8 * ns * pair_stats_grid(count));
+  return GPZB_OK;
+}
+
+int gpzb_pair_blocks(const void* const* orig, const void* const* rec, int dims, int prec, int rprec,
+                     uint64_t count, double eb_abs, uint32_t bs, uint32_t target, int64_t* orig_idx,
+                     int64_t* rec_idx, void* ws, uint64_t ws_bytes, void* stream, gpzb_result* res) {
+  clear_result(res);
+  int st = check_args(dims, prec, bs);
+  if (st) return res->status = st;
+  if ((rprec != GPZB_F32 && rprec != GPZB_F64) || target == 0 || (target & (target - 1)))
+    return res->status = GPZB_INVALID_ARGUMENT;
+  if (ws_bytes < sizeof(DevResult)) return res->status = GPZB_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (count == 0) return GPZB_OK;
+  PairParams P;
+  memset(&P, 0, sizeof(P));
+  for (int a = 0; a < dims; ++a) { P.orig[a] = orig[a]; P.rec[a] = rec[a]; }
+  P.count = count;
+  P.nblocks = nblocks_of(count, bs);
+  P.bs = bs;
+  P.target = target;
+  P.eb_abs = eb_abs;
+  P.orig_idx = orig_idx;
+  P.rec_idx = rec_idx;
+  P.res = reinterpret_cast<DevResult*>(ws);
+  cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(DevResult), s);
+  if (e != cudaSuccess) return res->status = cuda_status(e);
+  DISPATCH_DPR(dims, prec, rprec, launch_pair_blocks, P, s);
+  e = cudaGetLastError();
+  DevResult R;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&R, ws, sizeof(R), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return res->status = cuda_status(e);
+  res->nonfinite_mask = R.nonfinite_mask;
+  if (R.nonfinite_mask) {  // the Dataset invariant (model.py:75-77): original axes first
+    res->status = GPZB_DOMAIN_ERROR;
+    res->reason = R_NONFINITE;
+    const uint32_t m = (R.nonfinite_mask & 7) ? (R.nonfinite_mask & 7) : (R.nonfinite_mask >> 4);
+    res->axis = __builtin_ctz(m);
+    return res->status;
+  }
+  if (R.err_block) {
+    decode_err(R.err_block, &res->block, &res->axis, &res->reason);
+    res->status = status_of_reason(res->reason);
+    return res->status;
+  }
+  return GPZB_OK;
+}
+
+int gpzb_pair_stats(const void* const* orig, const void* const* rec, int dims, int prec, int rprec,
+                    uint64_t count, const int64_t* orig_idx, const int64_t* rec_idx, double eb_abs,
+                    uint64_t* viol, uint64_t viol_cap, void* ws, uint64_t ws_bytes, void* stream,
+                    double* stats, uint64_t* viol_count) {
+  uint64_t need = 0;
+  if (gpzb_pair_workspace(count, dims, &need) || ws_bytes < need) return GPZB_INVALID_ARGUMENT;
+  if ((prec != GPZB_F32 && prec != GPZB_F64) || (rprec != GPZB_F32 && rprec != GPZB_F64))
+    return GPZB_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t ns = 1 + 3 * (uint64_t)dims;
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  PairParams P;
+  memset(&P, 0, sizeof(P));
+  for (int a = 0; a < dims; ++a) { P.orig[a] = orig[a]; P.rec[a] = rec[a]; }
+  P.count = count;
+  P.eb_abs = eb_abs;
+  P.orig_idx = const_cast<int64_t*>(orig_idx);
+  P.rec_idx = const_cast<int64_t*>(rec_idx);
+  P.viol_count = reinterpret_cast<unsigned long long*>(base + align_up(sizeof(DevResult)));
+  P.out = reinterpret_cast<double*>(base + align_up(sizeof(DevResult)) + 8);
+  P.partial = reinterpret_cast<double*>(base + align_up(sizeof(DevResult)) + align_up(8 + 8 * ns));
+  P.viol = reinterpret_cast<unsigned long long*>(viol);
+  P.viol_cap = viol ? viol_cap : 0;
+  const unsigned grid = pair_stats_grid(count);
+  cudaError_t e = cudaMemsetAsync(P.viol_count, 0, 8, s);
+  if (e != cudaSuccess) return cuda_status(e);
+  DISPATCH_DPR(dims, prec, rprec, launch_pair_stats, P, grid, s);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(stats, P.out, 8 * ns, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(viol_count, P.viol_count, 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return cuda_status(e);
 }
 
 }  // extern "C"

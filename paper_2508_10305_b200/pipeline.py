@@ -267,9 +267,16 @@ def decompress(data, workers: int = 1) -> Dataset:
     """Reconstruct a dataset from container bytes (pipeline.py:160-205).
 
     Particles come back in sorted intra-block order unless the container
-    preserves order; block boundaries always match the original.
+    preserves order; block boundaries always match the original.  The axes
+    are numpy arrays over pinned host memory (PyTorch's caching host
+    allocator), filled by one device-to-host copy each.
     """
-    return decompress_device(data, workers).numpy()
+    ds = decompress_device(data, workers)
+    outs = [torch.empty(a.numel(), dtype=a.dtype, pin_memory=True) for a in ds.axes]
+    for o, a in zip(outs, ds.axes):
+        o.copy_(a, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return Dataset(axes=tuple(o.numpy() for o in outs), precision=ds.precision)
 
 
 def iter_decompressed_blocks(data) -> Iterator[list]:
