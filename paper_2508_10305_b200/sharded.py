@@ -51,6 +51,7 @@ class ShardedContainer:
     global_blocks: int
     local_blocks: int
     header: bytes            # global 46-byte header (every rank knows it)
+    global_payload: int = 0  # payload bytes over all ranks (file length - 46 - 8 (B + 1))
 
     @property
     def local_bytes(self) -> int:
@@ -170,7 +171,8 @@ def compress_device(ds: Dataset, cfg: CompressConfig, *, timing=None, hooks=None
     base = sum(totals[:rank])
     header = _header(ds.dims, ds.precision.value, cfg, float(res.eb_abs), g_count, g_blocks)
     return ShardedContainer(local=local, rank=rank, world=world, base=base, first_block=first_block,
-                            global_count=g_count, global_blocks=g_blocks, local_blocks=nb, header=header)
+                            global_count=g_count, global_blocks=g_blocks, local_blocks=nb, header=header,
+                            global_payload=sum(totals))
 
 
 def _comm_device():

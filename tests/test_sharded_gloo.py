@@ -67,7 +67,7 @@ class OracleHooks:
         return 0, L.Result(status=0, eb_abs=eb_abs), blob
 
 
-def _run(rank, world, port, case, q):
+def _run(rank, world, port, case, q, path=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -89,6 +89,18 @@ def _run(rank, world, port, case, q):
         except gz.GpzError as exc:
             q.put((rank, "err", type(exc).__name__, str(exc)))
             return
+        if case == "file":
+            from paper_2508_10305_b200 import gpzfile
+
+            gpzfile.write_sharded(path, sc)
+            if rank == 0:
+                with open(path, "rb") as f:
+                    got = f.read()
+                want = O.compress(full, O.Config(cfg.error_bound, mode.value))
+                q.put((rank, "ok", got == want, len(want)))
+            else:
+                q.put((rank, "ok", True, 0))
+            return
         blob = sharded.to_global_bytes(sc)
         if rank == 0:
             want = O.compress(full, O.Config(cfg.error_bound, mode.value))
@@ -107,19 +119,20 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("case", ["rel", "overflow"])
-def test_sharded_global_container_equals_single_process(case):
+@pytest.mark.parametrize("case", ["rel", "overflow", "file"])
+def test_sharded_global_container_equals_single_process(case, tmp_path):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_run, args=(r, 2, port, case, q)) for r in range(2)]
+    path = str(tmp_path / "sharded.gpz")
+    procs = [ctx.Process(target=_run, args=(r, 2, port, case, q, path)) for r in range(2)]
     for p in procs:
         p.start()
     out = [q.get(timeout=120) for _ in procs]
     for p in procs:
         p.join(timeout=60)
     out.sort()
-    if case == "rel":
+    if case in ("rel", "file"):
         assert out[0][1:3] == ("ok", True), out
         assert out[1][1] == "ok"
     else:
