@@ -1,0 +1,117 @@
+"""BASELINE.json configurations beyond the bench workload, at full size.
+
+configs[2]  LiDAR-style clustered point cloud, 500M points xyz f32, rel-eb 1e-4
+configs[3]  decompression sweep over rel-eb 1e-2 / 1e-3 / 1e-4 on 1B particles
+
+At these sizes the oracle cannot run end to end, so parity is checked by
+(1) sampled blocks of the GPU container against the oracle's per-block
+encoder and decoder (bit-exact bytes and values), (2) the size-independent
+properties: the offset table is consistent with the container length, and
+the whole reconstruction is within the bound under the reference's block
+pairing (K5, metrics.verify_bound semantics), (3) compression ratio = input
+bytes / container bytes with the container byte-exact per sampled block.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import gpz_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+gz = pytest.importorskip("paper_2508_10305_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def gen_lidar(n: int, seed: int):
+    """2.5-D terrain in scan-line order: jittered x/y lattice rows, z a smooth
+    height field plus sensor noise."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    w = int(np.ceil(np.sqrt(n)))
+    i = torch.arange(n, device="cuda", dtype=torch.int64)
+    f64 = torch.float64
+    x = (i % w).to(f64) * 0.05 + (torch.rand(n, generator=g, device="cuda", dtype=f64) * 2 - 1) * 0.01
+    y = (i // w).to(f64) * 0.05 + (torch.rand(n, generator=g, device="cuda", dtype=f64) * 2 - 1) * 0.01
+    z = 10.0 * torch.sin(x / 50.0) * torch.cos(y / 37.0) + 0.002 * torch.randn(n, generator=g, device="cuda",
+                                                                                  dtype=f64)
+    return [x.float(), y.float(), z.float()]
+
+
+def gen_clusters_dev(n: int, clusters: int, sigma: float, seed: int):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    centers = torch.rand(clusters, 3, generator=g, device="cuda", dtype=torch.float64)
+    out = []
+    for a in range(3):
+        assign = (torch.arange(n, device="cuda", dtype=torch.int64) * clusters) // n
+        v = centers[assign, a] + sigma * torch.randn(n, generator=g, device="cuda", dtype=torch.float64)
+        del assign
+        out.append(v.float())
+    return out
+
+
+def sampled_parity(axes, cfg, container, rec, picks):
+    n = axes[0].numel()
+    bs = cfg.block_size
+    nb = (n + bs - 1) // bs
+    head = container[:46].cpu().numpy().tobytes()
+    table = container[46: 46 + 8 * (nb + 1)].cpu().numpy().view("<u8")
+    pay0 = 46 + 8 * (nb + 1)
+    assert int(table[0]) == 0 and int(table[-1]) + pay0 == container.numel()
+    eb_abs = float(np.frombuffer(head[18:26], "<f8")[0])
+    oc = O.Config(cfg.error_bound, eb_mode=cfg.eb_mode.value, block_size=bs,
+                  target_segs_per_axis=cfg.target_segs_per_axis)
+    h = O.Header(3, O.F32, False, cfg.eb_mode.value, cfg.error_bound, eb_abs, bs, n, nb)
+    for i in picks:
+        sl = slice(i * bs, min((i + 1) * bs, n))
+        block = [a[sl].cpu().numpy() for a in axes]
+        want = O.encode_block(block, eb_abs, oc, O.F32)
+        got = container[pay0 + int(table[i]): pay0 + int(table[i + 1])].cpu().numpy().tobytes()
+        assert got == want, f"block {i}"
+        dec = O.decode_block(want, h)
+        for a in range(3):
+            assert np.array_equal(rec.axes[a][sl].cpu().numpy(), dec[a]), f"decode block {i}"
+    return eb_abs
+
+
+def _picks(nb, k=200, seed=0):
+    rng = np.random.default_rng(seed)
+    return sorted(set(rng.integers(0, nb, k).tolist()) | {0, nb - 1})
+
+
+def test_config2_lidar_500m_rel_1e4():
+    n = 500_000_000
+    axes = gen_lidar(n, 500)
+    ds = gz.Dataset.from_axes(axes)
+    cfg = gz.CompressConfig(error_bound=1e-4)
+    c = gz.compress_device(ds, cfg)
+    rec = gz.decompress_device(c)
+    nb = (n + 1023) // 1024
+    eb_abs = sampled_parity(axes, cfg, c, rec, _picks(nb))
+    assert eb_abs == gz.resolve_absolute_bound(ds, cfg)
+    rep = gz.verify_bound(ds, rec, eb_abs, cfg)
+    assert rep.ok and rep.max_err <= eb_abs and rep.checked == 3 * n
+    print(f"lidar 500M rel 1e-4: CR {ds.nbytes / c.numel():.3f}, max_err/eb {rep.max_err / eb_abs:.6f}")
+
+
+def test_config3_decompression_sweep_1b():
+    n = 1_000_000_000
+    axes = gen_clusters_dev(n, 32768, 0.002, 1000)
+    ds = gz.Dataset.from_axes(axes)
+    nb = (n + 1023) // 1024
+    for k, eb in enumerate((1e-2, 1e-3, 1e-4)):
+        cfg = gz.CompressConfig(error_bound=eb)
+        c = gz.compress_device(ds, cfg)
+        rec = gz.decompress_device(c)
+        eb_abs = sampled_parity(axes, cfg, c, rec, _picks(nb, 100, seed=k))
+        rep = gz.verify_bound(ds, rec, eb_abs, cfg)
+        assert rep.ok and rep.max_err <= eb_abs
+        print(f"1B clusters rel {eb:g}: CR {ds.nbytes / c.numel():.3f}")
+        del c, rec
+        torch.cuda.empty_cache()
