@@ -295,7 +295,7 @@ def main():
     dec_avg = statistics.mean(dec_ms) / 1e3 if dec_ms else float("nan")
     t_d = t_d or float("nan")
     rng_avg = statistics.mean(rng_ms) / 1e3 if rng_ms else float("nan")
-    roof = {"bound": "hbm", "kernel": "k_encode (K2)", "achieved": enc_bytes / enc_avg / 1e9, "peak": hbm,
+    roof = {"bound": "hbm", "kernel": "encode call: k_encode (K2) + k_scan_sizes + k_copy_payloads (K3)", "achieved": enc_bytes / enc_avg / 1e9, "peak": hbm,
             "unit": "GB/s", "frac": enc_bytes / enc_avg / 1e9 / hbm, "traffic": traffic,
             "algorithmic_bytes_per_launch": enc_bytes, "avg_launch_ms": enc_avg * 1e3,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
@@ -322,7 +322,7 @@ def main():
                    "input_checksum_rank0": checksum(pos + vel)},
         "compression_ratio": cr,
         "decompress": {"value": decomp_gbps, "unit": "GB/s", "ms_per_step": t_d / steps * 1e3,
-                       "roofline": {"bound": "hbm", "kernel": "k_decode (K4)",
+                       "roofline": {"bound": "hbm", "kernel": "decode call: k_decode_plan (K4a) + k_decode (K4)",
                                     "achieved": (local_in + statistics.mean(local_cont)) / dec_avg / 1e9,
                                     "peak": hbm, "unit": "GB/s",
                                     "frac": (local_in + statistics.mean(local_cont)) / dec_avg / 1e9 / hbm,
