@@ -45,7 +45,7 @@ struct __align__(16) DecRec {
   uint8_t chk_mask;   // bit a: reconstruction may be non-finite -> per-element check
   uint8_t pn_big;     // Π N > 2^32 (64-bit delinearisation)
   uint8_t pn_all;     // Π N >= 2^64 (every id in range)
-  uint8_t fast_body;  // 32-bit decode body applies (see k_decode); 2: with the midpoint table
+  uint8_t fast_body;  // 32-bit decode body applies (see k_decode); 2: with the midpoint table; 3: 32-bit q
   uint16_t lut1, lut2;  // fast_body 2: table offsets of axes 1 and 2 (axis 0 starts at 0)
   uint16_t lut_n;       // fast_body 2: table entries (Σ N_a 2^b_a)
 };
@@ -236,6 +236,11 @@ __global__ void __launch_bounds__(256) k_decode_plan(const DecParams P) {
     if (tot <= (uint64_t)kLutEntries / (F64 ? 2 : 1) && U <= GPZB_LUT_UMAX) {
       rec.fast_body = 2;
       rec.lut_n = (uint16_t)tot;
+    } else {
+      bool q31 = true;
+#pragma unroll
+      for (int a = 0; a < D; ++a) q31 = q31 && rec.b[a] <= 30 && ((uint64_t)rec.N[a] << rec.b[a]) <= (1ull << 31);
+      if (q31) rec.fast_body = 3;  // 32-bit bin indices (k_decode fast body)
     }
   }
   P.rec[blk] = rec;
@@ -361,7 +366,8 @@ __device__ __forceinline__ void decode_fast(const DecParams& P, DecSmem& sm, con
     const uint32_t used = cnt * w, nb = (used + 7) >> 3;
     if (w && cnt && (used & 7) && (pb[st + nb - 1] >> (used & 7))) fl |= 1u << tid;
   }
-  unsigned long long dsum = 0, csum = 0;
+  unsigned long long dsum = 0;
+  uint32_t csum = 0;
   uint32_t dl[kItems], cn[kItems];
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
@@ -378,11 +384,18 @@ __device__ __forceinline__ void decode_fast(const DecParams& P, DecSmem& sm, con
 #pragma unroll
   for (int k = 0; k < kItems; ++k) off[k] = get_bits32(sm.words, pbit + 8 * so + (p0 + k) * wo, wo);
   const bool lut = rec->fast_body == 2;
-  unsigned long long dtot, ctot;
-  block_excl_scan2(dsum, csum, dtot, ctot, sm.scan);
+  // one u64 scan for both sums: Σ deltas < 1024 * 2^32 = 2^42 (widths <= 32)
+  // in the low 43 bits, run lengths above them, clamped per thread at 1025
+  // (a valid block sums to exactly 1024, so clamping never hides an error)
+  constexpr int kDBits = 43;
+  constexpr unsigned long long kDMask = (1ull << kDBits) - 1;
+  unsigned long long tot;
+  const unsigned long long ex =
+      block_excl_scan<unsigned long long>(((unsigned long long)min(csum, 1025u) << kDBits) | dsum, tot, sm.scan);
+  const unsigned long long ctot = tot >> kDBits;
   {
-    uint64_t prev = dsum;
-    uint32_t cex = (uint32_t)csum;
+    uint64_t prev = ex & kDMask;
+    uint32_t cex = (uint32_t)(ex >> kDBits);
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
       const uint32_t r = p0 + j;
@@ -487,7 +500,7 @@ __device__ __forceinline__ void decode_fast(const DecParams& P, DecSmem& sm, con
     }
   } else {
   double lo[D], w[D];
-  uint32_t bsh[D], shifts[D], Nn[D], mgm[D], mgl[D];
+  uint32_t bsh[D], shifts[D], Nn[D], mgm[D], mgl[D], omask[D];
   {
     uint32_t s = 0;
 #pragma unroll
@@ -495,6 +508,7 @@ __device__ __forceinline__ void decode_fast(const DecParams& P, DecSmem& sm, con
       lo[a] = rec->lo[a];
       w[a] = rec->w[a];
       bsh[a] = rec->b[a];
+      omask[a] = bsh[a] >= 32 ? 0xffffffffu : (1u << bsh[a]) - 1u;
       shifts[a] = s;
       s += bsh[a];
       Nn[a] = rec->N[a];
@@ -502,6 +516,28 @@ __device__ __forceinline__ void decode_fast(const DecParams& P, DecSmem& sm, con
       mgl[a] = rec->mg_l[a];
     }
   }
+  if (rec->fast_body == 3) {
+    // every bin index < 2^31 (K4a): 32-bit q and the 2^51 magic constant from one word
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      uint32_t rest = (uint32_t)sm.uniq[run[k]];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        uint32_t sa;
+        if (a + 1 < D) {
+          const uint32_t qd = magic_div(rest, mgm[a], mgl[a]);
+          sa = rest - qd * Nn[a];
+          rest = qd;
+        } else {
+          sa = rest;
+        }
+        const uint32_t q = (sa << bsh[a]) | ((off[k] >> shifts[a]) & omask[a]);
+        const double h = __hiloint2double(0x43200000, (int)(2u * q + 1u));
+        const double aq = __dsub_rn(h, 2251799813685248.0);
+        vals[a][k] = (T)__dadd_rn(lo[a], __dmul_rn(aq, w[a]));
+      }
+    }
+  } else {
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
     uint32_t rest = (uint32_t)sm.uniq[run[k]];
@@ -522,6 +558,7 @@ __device__ __forceinline__ void decode_fast(const DecParams& P, DecSmem& sm, con
       const double aq = __dsub_rn(h, 2251799813685248.0);
       vals[a][k] = (T)__dadd_rn(lo[a], __dmul_rn(aq, w[a]));
     }
+  }
   }
   }
   const uint64_t idx0 = (P.out_offsets ? P.out_offsets[blk] : blk * (uint64_t)P.bs) + p0;
