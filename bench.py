@@ -188,16 +188,28 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     n = args.particles
+    if world > 1 and rank < world - 1:
+        # shards must be block-aligned (sharded.py): every rank but the last
+        # rounds its particle count up to whole 1024-particle blocks
+        n = (n + 1023) // 1024 * 1024
 
     if args.impl == "reference":
         return run_reference(args, world, rank)
 
+    # GPZB_BENCH_SHARE_GPU=1: every rank on cuda:0 over gloo (exercises the
+    # sharded path on a one-GPU box; never used for reported numbers)
+    share = os.environ.get("GPZB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     import paper_2508_10305_b200 as gz
     from paper_2508_10305_b200 import sharded
 
@@ -251,16 +263,17 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([t_c, t_d], dtype=torch.float64, device=dev)
+        cdev = "cpu" if share else dev
+        t = torch.tensor([t_c, t_d], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_c, t_d = t.tolist()
-        z = torch.tensor([float(sum(sizes))], dtype=torch.float64, device=dev)
+        z = torch.tensor([float(sum(sizes)), float(in_bytes)], dtype=torch.float64, device=cdev)
         dist.all_reduce(z)
-        total_container = z.item()
+        total_container, job_bytes = z.tolist()
     else:
         total_container = float(sum(sizes))
+        job_bytes = float(in_bytes)
     steps = args.steps
-    job_bytes = in_bytes * world
     comp_gbps = job_bytes * steps / t_c / 1e9
     decomp_gbps = job_bytes * steps / t_d / 1e9
     cr = job_bytes / total_container

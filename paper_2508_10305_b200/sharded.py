@@ -59,10 +59,15 @@ class ShardedContainer:
 
 
 def _allreduce_max_words(words: torch.Tensor) -> None:
-    """MAX all-reduce of u64 order-preserving words stored as int64."""
-    words ^= _I64_MIN
-    dist.all_reduce(words, op=dist.ReduceOp.MAX)
-    words ^= _I64_MIN
+    """MAX all-reduce of u64 order-preserving words stored as int64 (in place;
+    over NCCL the device words are reduced directly, otherwise via the host)."""
+    dev = _comm_device()
+    t = words if words.device == dev else words.to(dev)
+    t ^= _I64_MIN
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t ^= _I64_MIN
+    if t is not words:
+        words.copy_(t)
 
 
 def _gather_ints(v: int, device) -> list[int]:

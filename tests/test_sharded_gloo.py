@@ -139,3 +139,55 @@ def test_sharded_global_container_equals_single_process(case, tmp_path):
         # both ranks raise the same first error, with the global block index
         for r in out:
             assert r[1] == "err" and r[2] == "WidthOverflow" and r[3].startswith("block 3"), out
+
+
+def _run_cuda(rank, world, port, q, path):
+    """Both ranks on cuda:0 (gloo for the scalar exchanges): the product CUDA
+    hooks of sharded.compress_device, exactly as under torchrun with NCCL."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2508_10305_b200 as gz
+        from paper_2508_10305_b200 import gpzfile, sharded
+
+        full = O.gen_clusters(400_000, dims=3, seed=21)
+        cut = 196 * 1024
+        sl = slice(0, cut) if rank == 0 else slice(cut, None)
+        ds = gz.Dataset.from_axes([torch.from_numpy(a[sl].copy()).cuda() for a in full])
+        cfg = gz.CompressConfig(error_bound=1e-3)
+        sc = sharded.compress_device(ds, cfg)
+        blob = sharded.to_global_bytes(sc)
+        gpzfile.write_sharded(path, sc)
+        rec = sharded.decompress_device(sc)
+        if rank == 0:
+            want = gz.compress(gz.Dataset.from_axes(full), cfg)
+            with open(path, "rb") as f:
+                disk = f.read()
+            full_rec = gz.decompress(want)
+            ok_rec = all(np.array_equal(r.cpu().numpy(), w[:cut]) for r, w in zip(rec.axes, full_rec.axes))
+            q.put((rank, blob == want, disk == want, ok_rec))
+        else:
+            full_rec = gz.decompress(gz.compress(gz.Dataset.from_axes(full), cfg))
+            ok_rec = all(np.array_equal(r.cpu().numpy(), w[cut:]) for r, w in zip(rec.axes, full_rec.axes))
+            q.put((rank, True, True, ok_rec))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_cuda_hooks_two_ranks_one_gpu(tmp_path):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    path = str(tmp_path / "sharded_cuda.gpz")
+    procs = [ctx.Process(target=_run_cuda, args=(r, 2, port, q, path)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert out == [(0, True, True, True), (1, True, True, True)], out
