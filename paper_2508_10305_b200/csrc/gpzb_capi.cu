@@ -17,6 +17,10 @@ using namespace gpzb;
 
 namespace {
 
+#ifndef GPZB_K1_CTAS
+#define GPZB_K1_CTAS 16
+#endif
+
 constexpr uint64_t kAlign = 256;
 inline uint64_t align_up(uint64_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
 
@@ -89,8 +93,13 @@ void clear_result(gpzb_result* r) {
 
 template <int D, bool F64>
 void launch_range(const EncParams& P, cudaStream_t s) {
+#ifdef GPZB_K1_CTA
   const uint64_t grid = std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * 8);
   k_range<D, typename std::conditional<F64, double, float>::type><<<(unsigned)grid, kThreads, 0, s>>>(P);
+#else
+  const uint64_t grid = std::min<uint64_t>((P.nblocks + kWarps - 1) / kWarps, (uint64_t)sm_count() * GPZB_K1_CTAS);
+  k_range_w<D, typename std::conditional<F64, double, float>::type><<<(unsigned)grid, kThreads, 0, s>>>(P);
+#endif
 }
 
 template <int D, bool F64>

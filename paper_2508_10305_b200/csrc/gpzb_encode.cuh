@@ -155,27 +155,36 @@ __device__ __forceinline__ void block_bounds(const T (&x)[D][kItems], int n, int
 // per-block bounds for K2, and the Dataset finiteness check (model.py:75-77).
 template <int D, typename T>
 __global__ void __launch_bounds__(kThreads) k_range(const EncParams P) {
-  __shared__ __align__(16) double ws[3 * 2 * kWarps];
+  __shared__ __align__(16) double ws[2][3 * 2 * kWarps];
   const int p0 = threadIdx.x * kItems;
   double run_lo = __longlong_as_double(0x7ff0000000000000ll), run_hi = -run_lo;
   uint32_t nf_all = 0;
-  for (uint64_t blk = blockIdx.x; blk < P.nblocks; blk += gridDim.x) {
-    const uint64_t first = blk * (uint64_t)P.bs;
+  // two blocks per iteration: both loads are in flight before either reduction
+  for (uint64_t blk = blockIdx.x; blk < P.nblocks; blk += 2ull * gridDim.x) {
+    const uint64_t blk2 = blk + gridDim.x;
+    const bool has2 = blk2 < P.nblocks;
+    T x[2][D][kItems];
+    const uint64_t first = blk * (uint64_t)P.bs, first2 = blk2 * (uint64_t)P.bs;
     const int n = (int)min((uint64_t)P.bs, P.count - first);
-    T x[D][kItems];
-    load_particles<D, T>(P, first, n, p0, x);
-    double lo[D], hi[D];
-    uint32_t nf;
-    block_bounds<D, T>(x, n, p0, lo, hi, nf, ws);
-    nf_all |= nf;
-    if (threadIdx.x == 0) {
-      T* out = reinterpret_cast<T*>(const_cast<void*>(P.bounds)) + blk * 2 * D;
+    const int n2 = has2 ? (int)min((uint64_t)P.bs, P.count - first2) : 0;
+    load_particles<D, T>(P, first, n, p0, x[0]);
+    if (has2) load_particles<D, T>(P, first2, n2, p0, x[1]);
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        out[2 * a] = (T)lo[a];
-        out[2 * a + 1] = (T)hi[a];
-        run_lo = fmin(run_lo, lo[a]);
-        run_hi = fmax(run_hi, hi[a]);
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && !has2) break;
+      double lo[D], hi[D];
+      uint32_t nf;
+      block_bounds<D, T>(x[h], h ? n2 : n, p0, lo, hi, nf, ws[h]);
+      nf_all |= nf;
+      if (threadIdx.x == 0) {
+        T* out = reinterpret_cast<T*>(const_cast<void*>(P.bounds)) + (h ? blk2 : blk) * 2 * D;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          out[2 * a] = (T)lo[a];
+          out[2 * a + 1] = (T)hi[a];
+          run_lo = fmin(run_lo, lo[a]);
+          run_hi = fmax(run_hi, hi[a]);
+        }
       }
     }
   }
@@ -188,6 +197,136 @@ __global__ void __launch_bounds__(kThreads) k_range(const EncParams P) {
   if ((threadIdx.x & 31) == 0 && nf_all) atomicOr(&P.res->nonfinite_mask, nf_all);
 }
 
+// K1, warp per block: each warp streams whole blocks (16-byte loads, eight
+// per lane and axis in flight, no CTA barriers) and reduces them with warp
+// primitives; one atomic per CTA for the joint range.
+template <int D, typename T>
+__global__ void __launch_bounds__(kThreads) k_range_w(const EncParams P) {
+  __shared__ double cta_lo[kWarps], cta_hi[kWarps];
+  __shared__ uint32_t cta_nf[kWarps];
+  constexpr int VE = 16 / sizeof(T);  // elements per 16-byte load
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t gw = (uint64_t)blockIdx.x * kWarps + wid, nw = (uint64_t)gridDim.x * kWarps;
+  double run_lo = __longlong_as_double(0x7ff0000000000000ll), run_hi = -run_lo;
+  uint32_t nf_all = 0;
+  for (uint64_t blk = gw; blk < P.nblocks; blk += nw) {
+    const uint64_t first = blk * (uint64_t)P.bs;
+    const uint32_t n = (uint32_t)min((uint64_t)P.bs, P.count - first);
+    const bool vec = P.vec && (n % VE) == 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const T* base = reinterpret_cast<const T*>(P.axes[a]) + first;
+      double lo, hi;
+      uint32_t nf = 0;
+      if constexpr (sizeof(T) == 4) {
+        // float: 32-bit order-preserving keys (fkey), warp REDUX
+        int mn = 0x7fffffff, mx = (int)0x80000000;
+        uint32_t ex = 0;  // OR of exponent fields == 0xff marks inf / nan
+        if (vec) {
+          const uint32_t nv = n / VE;
+          constexpr int U = 8;
+          for (uint32_t c0 = 0; c0 < nv; c0 += 32 * U) {
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t c = c0 + u * 32 + lane;
+              v[u] = c < nv ? __ldcs(reinterpret_cast<const uint4*>(base) + c) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              if (c0 + u * 32 + lane < nv) {
+                const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const int k = fkey(__uint_as_float(w4[j]));
+                  mn = min(mn, k);
+                  mx = max(mx, k);
+                  ex |= ((w4[j] & 0x7f800000u) == 0x7f800000u);
+                }
+              }
+            }
+          }
+        } else {
+          for (uint32_t p = lane; p < n; p += 32) {
+            const float f = __ldcs(base + p);
+            const int k = fkey(f);
+            mn = min(mn, k);
+            mx = max(mx, k);
+            ex |= !isfinite(f);
+          }
+        }
+        mn = __reduce_min_sync(kFull, mn);
+        mx = __reduce_max_sync(kFull, mx);
+        nf = __reduce_or_sync(kFull, ex);
+        lo = (double)fkey_inv(mn);
+        hi = (double)fkey_inv(mx);
+      } else {
+        unsigned long long mn = ~0ull, mx = 0ull;  // order-preserving keys
+        if (vec) {
+          const uint32_t nv = n / VE;
+          constexpr int U = 8;
+          for (uint32_t c0 = 0; c0 < nv; c0 += 32 * U) {
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t c = c0 + u * 32 + lane;
+              v[u] = c < nv ? __ldcs(reinterpret_cast<const uint4*>(base) + c) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              if (c0 + u * 32 + lane < nv) {
+                const double* e = reinterpret_cast<const double*>(&v[u]);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                  if (!isfinite(e[j])) nf = 1;
+                  const unsigned long long k = ukey(e[j]);
+                  mn = min(mn, k);
+                  mx = max(mx, k);
+                }
+              }
+            }
+          }
+        } else {
+          for (uint32_t p = lane; p < n; p += 32) {
+            const double f = __ldcs(base + p);
+            if (!isfinite(f)) nf = 1;
+            const unsigned long long k = ukey(f);
+            mn = min(mn, k);
+            mx = max(mx, k);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          mn = min(mn, __shfl_xor_sync(kFull, mn, o));
+          mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+        }
+        nf = __reduce_or_sync(kFull, nf);
+        lo = ukey_inv(mn);
+        hi = ukey_inv(mx);
+      }
+      if (lane == 0) {
+        T* out = reinterpret_cast<T*>(const_cast<void*>(P.bounds)) + blk * 2 * D;
+        out[2 * a] = (T)lo;
+        out[2 * a + 1] = (T)hi;
+      }
+      nf_all |= nf << a;
+      run_lo = fmin(run_lo, lo);
+      run_hi = fmax(run_hi, hi);
+    }
+  }
+  if (lane == 0) { cta_lo[wid] = run_lo; cta_hi[wid] = run_hi; cta_nf[wid] = nf_all; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double lo = cta_lo[0], hi = cta_hi[0];
+    uint32_t nf = cta_nf[0];
+    for (int w = 1; w < kWarps; ++w) { lo = fmin(lo, cta_lo[w]); hi = fmax(hi, cta_hi[w]); nf |= cta_nf[w]; }
+    if (lo <= hi) {
+      atomicMax(&P.res->range_w[0], ukey(-lo));
+      atomicMax(&P.res->range_w[1], ukey(hi));
+    }
+    if (nf) atomicOr(&P.res->nonfinite_mask, nf);
+  }
+}
 
 // ------------------------------------------------------------------ K1.5
 // Per-block geometry record: everything the 32-bit encoder needs, so K2
