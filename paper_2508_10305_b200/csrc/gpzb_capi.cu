@@ -8,6 +8,7 @@
 #include <cstring>
 
 #include "gpzb_decode.cuh"
+#include "gpzb_decode_warp.cuh"
 #include "gpzb_encode.cuh"
 #include "gpzb_encode_narrow.cuh"
 #include "gpzb_encode_wide.cuh"
@@ -136,12 +137,22 @@ void launch_encode(const EncParams& P, bool wide, cudaStream_t s) {
 template <int D, bool F64>
 void launch_decode(const DecParams& P, bool pres, cudaStream_t s) {
   const unsigned pgrid = (unsigned)((P.nblocks + 255) / 256);
+  const unsigned lgrid = (unsigned)std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * GPZB_K4_MINB);
   if (pres) {
     k_decode_plan<D, F64, true><<<pgrid, 256, 0, s>>>(P);
-    k_decode<D, F64, true><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
+    k_decode_list<D, F64, true><<<lgrid, kThreads, 0, s>>>(P, P.list);
   } else {
     k_decode_plan<D, F64, false><<<pgrid, 256, 0, s>>>(P);
-    k_decode<D, F64, false><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_decode_warp<D, F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kWarpDecSmemBytes);
+      attr = true;
+    }
+    const unsigned wgrid = (unsigned)std::min<uint64_t>((P.nblocks + kWarpDecWarps - 1) / kWarpDecWarps,
+                                                        (uint64_t)sm_count() * 3);
+    k_decode_warp<D, F64><<<wgrid, 32 * kWarpDecWarps, kWarpDecSmemBytes, s>>>(P);
+    k_decode_list<D, F64, false><<<lgrid, kThreads, 0, s>>>(P, P.list);
   }
 }
 
@@ -302,7 +313,7 @@ int gpzb_compress_workspace(uint64_t count, int dims, int prec, uint32_t bs, uin
 }
 
 int gpzb_decompress_workspace(const gpzb_header* h, uint64_t* ws_bytes) {
-  *ws_bytes = align_up(sizeof(DevResult)) + align_up(h->block_count * sizeof(DecRec));
+  *ws_bytes = align_up(sizeof(DevResult)) + align_up(h->block_count * sizeof(DecRec)) + align_up(4 * h->block_count);
   return GPZB_OK;
 }
 
@@ -527,8 +538,10 @@ int gpzb_decompress_async(const uint8_t* c, uint64_t len, const gpzb_header* h, 
   P.out_cap = out_cap;
   P.out_offsets = out_offsets;
   P.res = reinterpret_cast<DevResult*>(ws);
-  if (ws_bytes < align_up(sizeof(DevResult)) + h->block_count * sizeof(DecRec)) return GPZB_INVALID_ARGUMENT;
+  const uint64_t list_off = align_up(sizeof(DevResult)) + align_up(h->block_count * sizeof(DecRec));
+  if (ws_bytes < list_off + 4 * h->block_count) return GPZB_INVALID_ARGUMENT;
   P.rec = reinterpret_cast<DecRec*>(static_cast<uint8_t*>(ws) + align_up(sizeof(DevResult)));
+  P.list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + list_off);
   DISPATCH_DP(h->dims, h->precision, launch_decode, P, h->preserve_order != 0, s);
   return cuda_status(cudaGetLastError());
 }

@@ -38,7 +38,7 @@ struct __align__(16) DecRec {
   uint8_t b[3];       // log2(m)
   uint8_t mg_l[3];    // magic shift
   uint8_t wd, wc, wo, wr;
-  uint8_t kind;       // 0 decode, 1 skip (error already reported / table error)
+  uint8_t kind;       // 0 CTA decoder, 1 skip (error already reported / table error), 2 warp decoder
   uint8_t sumb;
   uint8_t fast_mask;  // bit a: magic-constant midpoint valid (q < 2^51)
   uint8_t geo_bits;   // bit 2a: axis range overflow, bit 2a+1: N inconsistent
@@ -63,6 +63,7 @@ struct DecParams {
   const uint64_t* out_offsets;  // null: block i starts at i*bs
   DevResult* res;
   DecRec* rec;
+  uint32_t* list;          // K4a: blocks for the CTA decoder (count in res->wide_count)
 };
 
 constexpr int kDecStageWords = 5120;  // 20 KB payload window (legit blocks <= 19.2 KB)
@@ -241,6 +242,17 @@ __global__ void __launch_bounds__(256) k_decode_plan(const DecParams P) {
 #pragma unroll
       for (int a = 0; a < D; ++a) q31 = q31 && rec.b[a] <= 30 && ((uint64_t)rec.N[a] << rec.b[a]) <= (1ull << 31);
       if (q31) rec.fast_body = 3;  // 32-bit bin indices (k_decode fast body)
+    }
+  }
+  // route: the warp decoder (K4w) takes fast-body blocks whose payload
+  // window fits its 4 KB stage; the CTA decoder gets the rest via the list
+  {
+    const uint32_t al = (uint32_t)((uintptr_t)(P.c + P.table_end + e0) & 15);
+    const uint32_t plen = rec.so + ((kMaxBs * (uint32_t)rec.wo + 7) >> 3);
+    if (rec.fast_body && al + plen + 16 <= 4096u) {
+      rec.kind = 2;
+    } else if (P.list) {
+      P.list[atomicAdd(&R->wide_count, 1u)] = (uint32_t)blk;
     }
   }
   P.rec[blk] = rec;

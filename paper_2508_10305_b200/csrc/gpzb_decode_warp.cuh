@@ -1,0 +1,265 @@
+// K4w: warp-per-block decoder for the common blocks.
+//
+// The CTA decoder (k_decode, 256 threads x 4 particles) pays its per-thread
+// fixed costs — window load, two block scans, barriers, record loads —
+// over only four particles and four runs per thread.  Here one warp owns a
+// whole 1024-particle block: 32 runs and 32 particles per lane, warp scans
+// instead of block scans, no CTA barriers, so the fixed cost is spread over
+// 8x more work and independent warps never wait for each other.
+//
+// Eligible blocks (K4a marks them kind = 2): the fast body (full block,
+// stream widths <= 32, Σ log2 m <= 32, Π N <= 2^32, finite reconstruction,
+// no rank stream) whose payload window fits kWinBytes.  Everything else goes
+// to the CTA decoder through K4a's list.  Checks and their order are those
+// of decode_fast (pipeline.py:106-157 semantics; lowest bit = first failure).
+#pragma once
+
+#include "gpzb_decode.cuh"
+
+namespace gpzb {
+
+constexpr int kWinBytes = 4096;            // payload window per warp
+constexpr int kWarpDecWarps = 8;           // warps per CTA
+struct WarpDecSmem {
+  uint32_t win[kWinBytes / 4 + 8];
+  uint32_t uniq[kMaxBs];
+  uint32_t rstart[kMaxBs / 32];
+};
+constexpr size_t kWarpDecSmemBytes = sizeof(WarpDecSmem) * kWarpDecWarps;
+
+// The particle phase of K4w: 8 chunks of 128 positions, four consecutive
+// per lane (one 16-byte store per axis and chunk).  Q32: every bin index
+// < 2^31, so the 2^51 magic midpoint comes from one 32-bit word.
+template <int D, bool F64, bool Q32>
+__device__ __forceinline__ uint32_t warp_particles(const DecParams& P, const WarpDecSmem& sm, uint64_t blk,
+                                                   uint64_t idx_base, int lane, uint32_t wpre, uint32_t pbit,
+                                                   uint32_t so, uint32_t wo, uint32_t sb, const double (&lo)[D],
+                                                   const double (&w)[D], const uint32_t (&bsh)[D],
+                                                   const uint32_t (&shifts)[D], const uint32_t (&Nn)[D],
+                                                   const uint32_t (&mgm)[D], const uint32_t (&mgl)[D],
+                                                   const uint32_t (&omask)[D]) {
+  using T = typename std::conditional<F64, double, float>::type;
+  uint32_t offbad = 0;
+  const uint32_t omask4 = wo >= 32 ? 0xffffffffu : (1u << wo) - 1u;
+#pragma unroll 1
+  for (int c = 0; c < kMaxBs / 128; ++c) {
+    const uint32_t p0 = c * 128 + 4 * lane;
+    const uint32_t wsel = p0 >> 5;  // the four share one map word
+    const uint32_t word = sm.rstart[wsel];
+    const uint32_t base = __shfl_sync(kFull, wpre, wsel);
+    // the four offsets are adjacent in the stream: one or two 64-bit windows
+    uint32_t offs[4];
+    {
+      const uint32_t pos = pbit + 8 * so + p0 * wo;
+      const uint32_t* q = sm.win + (pos >> 5);
+      const uint32_t sh = pos & 31;
+      const uint64_t lo64 = (((uint64_t)q[1] << 32) | q[0]) >> sh | (sh ? (uint64_t)q[2] << (64 - sh) : 0ull);
+      if (4 * wo + 0 <= 64) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) offs[k] = (uint32_t)(lo64 >> (k * wo)) & omask4;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) offs[k] = get_bits32(sm.win, pos + k * wo, wo);
+      }
+    }
+    T vals[D][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t b = (p0 + k) & 31;
+      const uint32_t run = base + __popc(word & (0xffffffffu >> (31 - b))) - 1;
+      const uint32_t off = offs[k];
+      if (sb < 32) offbad |= off >> sb;  // quantizer.py:264-265
+      uint32_t rest = sm.uniq[run];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        uint32_t sa;
+        if (a + 1 < D) {
+          const uint32_t qd = magic_div(rest, mgm[a], mgl[a]);
+          sa = rest - qd * Nn[a];
+          rest = qd;
+        } else {
+          sa = rest;
+        }
+        const uint32_t oa = (off >> shifts[a]) & omask[a];
+        double h;
+        if constexpr (Q32) {
+          h = __hiloint2double(0x43200000, (int)(2u * ((sa << bsh[a]) | oa) + 1u));
+        } else {
+          const uint64_t qq = ((uint64_t)sa << bsh[a]) | oa;
+          h = __longlong_as_double((long long)(0x4320000000000000ull + 2 * qq + 1));
+        }
+        // RN(q + 0.5) exactly (2^51 magic), then lo + (q + 0.5) w (quantizer.py:132-139)
+        const double aq = __dsub_rn(h, 2251799813685248.0);
+        vals[a][k] = (T)__dadd_rn(lo[a], __dmul_rn(aq, w[a]));
+      }
+    }
+    const uint64_t idx0 = idx_base + p0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      T* out = reinterpret_cast<T*>(P.out[a]);
+      if (idx0 + 4 <= P.out_cap && ((reinterpret_cast<uintptr_t>(out + idx0) & 15) == 0)) {
+        if constexpr (sizeof(T) == 4) {
+          __stcs(reinterpret_cast<float4*>(out + idx0), make_float4(vals[a][0], vals[a][1], vals[a][2], vals[a][3]));
+        } else {
+          __stcs(reinterpret_cast<double2*>(out + idx0), make_double2(vals[a][0], vals[a][1]));
+          __stcs(reinterpret_cast<double2*>(out + idx0) + 1, make_double2(vals[a][2], vals[a][3]));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (idx0 + k < P.out_cap) out[idx0 + k] = vals[a][k];
+      }
+    }
+  }
+  return offbad;
+}
+
+template <int D, bool F64>
+__global__ void __launch_bounds__(32 * kWarpDecWarps, 3) k_decode_warp(const DecParams P) {
+  using T = typename std::conditional<F64, double, float>::type;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpDecSmem& sm = reinterpret_cast<WarpDecSmem*>(dsm)[wid];
+  DevResult* R = P.res;
+  const uint8_t* cend = P.c + P.len;
+
+  for (uint64_t blk = (uint64_t)blockIdx.x * kWarpDecWarps + wid; blk < P.nblocks;
+       blk += (uint64_t)gridDim.x * kWarpDecWarps) {
+    const DecRec* rec = P.rec + blk;
+    if (rec->kind != 2) continue;  // warp-uniform
+    const uint32_t U = rec->U;
+    const uint32_t wd = rec->wd, wc = rec->wc, wo = rec->wo;
+    const uint32_t sd = rec->sd, sc = rec->sc, so = rec->so;
+    const uint8_t* pay = P.c + P.table_end + rec->e0;
+    const uint32_t al = (uint32_t)((uintptr_t)pay & 15);
+    const uint32_t plen = so + ((kMaxBs * wo + 7) >> 3);
+    {  // payload window: 16-byte chunks, edges bytewise
+      const uint8_t* g16 = pay - al;
+      const uint32_t nch = (al + plen + 15) >> 4;
+      for (uint32_t ch = lane; ch < nch; ch += 32) {
+        const uint8_t* src = g16 + 16 * ch;
+        uint4 v;
+        if (src >= P.c && src + 16 <= cend) {
+          v = __ldcs(reinterpret_cast<const uint4*>(src));
+        } else {
+          uint32_t w[4] = {0, 0, 0, 0};
+          for (int j = 0; j < 16; ++j)
+            if (src + j >= P.c && src + j < cend) w[j >> 2] |= (uint32_t)src[j] << (8 * (j & 3));
+          v = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        reinterpret_cast<uint4*>(sm.win)[ch] = v;
+      }
+      sm.win[((nch * 16) >> 2) + lane % 4] = 0;  // get_bits32 may read one word past the end
+      sm.rstart[lane] = 0;
+    }
+    __syncwarp();
+    const uint8_t* pb = reinterpret_cast<const uint8_t*>(sm.win) + al;
+    const uint32_t pbit = 8 * al;
+    uint32_t fl = 0;
+    if (lane < 3) {  // zero padding (codec.py:147-148)
+      const uint32_t cnt = lane < 2 ? U : (uint32_t)kMaxBs;
+      const uint32_t w = lane == 0 ? wd : lane == 1 ? wc : wo;
+      const uint32_t st = lane == 0 ? sd : lane == 1 ? sc : so;
+      const uint32_t used = cnt * w, nb = (used + 7) >> 3;
+      if (w && cnt && (used & 7) && (pb[st + nb - 1] >> (used & 7))) fl |= 1u << lane;
+    }
+    // ---- runs: lane l owns runs [l*RPL, (l+1)*RPL)
+    const uint32_t RPL = (U + 31) >> 5;
+    const uint32_t r0 = lane * RPL, r1 = min(U, r0 + RPL);
+    unsigned long long dsum = 0;
+    uint32_t csum = 0;
+    for (uint32_t r = r0; r < r1; ++r) {
+      dsum += get_bits32(sm.win, pbit + 8 * sd + r * wd, wd);
+      csum += get_bits32(sm.win, pbit + 8 * sc + r * wc, wc);
+    }
+    // packed warp scan (Σ deltas < 2^42 in the low 43 bits; run lengths,
+    // clamped per lane at 1025, above them: a valid block sums to 1024)
+    constexpr int kDBits = 43;
+    constexpr unsigned long long kDMask = (1ull << kDBits) - 1;
+    const unsigned long long mine = ((unsigned long long)min(csum, 1025u) << kDBits) | dsum;
+    unsigned long long incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const unsigned long long ctot = __shfl_sync(kFull, incl, 31) >> kDBits;
+    {
+      const unsigned long long ex = incl - mine;
+      uint64_t prev = ex & kDMask;
+      uint32_t cex = (uint32_t)(ex >> kDBits);
+      for (uint32_t r = r0; r < r1; ++r) {
+        const uint32_t dl = get_bits32(sm.win, pbit + 8 * sd + r * wd, wd);
+        const uint32_t cn = get_bits32(sm.win, pbit + 8 * sc + r * wc, wc);
+        const uint64_t u = prev + dl;
+        if (r > 0 && u <= prev) fl |= 1u << 3;  // pipeline.py:116-117
+        if (cn < 1) fl |= 1u << 4;              // pipeline.py:118-119
+        if (u >= rec->PN) fl |= 1u << 13;       // quantizer.py:262-263
+        sm.uniq[r] = (uint32_t)u;
+        if (cex < (uint32_t)kMaxBs) red_or_shared(&sm.rstart[cex >> 5], 1u << (cex & 31));
+        cex += cn;
+        prev = u;
+      }
+    }
+    if (ctot != (unsigned long long)kMaxBs) fl |= 1u << 5;  // pipeline.py:120-123
+    fl = __reduce_or_sync(kFull, fl);
+    if (fl) {
+      if (lane == 0) report_decode_error(R, blk, fl);
+      __syncwarp();
+      continue;
+    }
+    __syncwarp();
+    // ---- run-start map prefix: lane w holds the starts before word w
+    const uint32_t wcount = __popc(sm.rstart[lane]);
+    uint32_t wpre = wcount;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, wpre, o);
+      if (lane >= o) wpre += y;
+    }
+    wpre -= wcount;
+    // ---- geometry constants (warp-uniform)
+    double lo[D], w[D];
+    uint32_t bsh[D], shifts[D], Nn[D], mgm[D], mgl[D], omask[D];
+    {
+      uint32_t s = 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        lo[a] = rec->lo[a];
+        w[a] = rec->w[a];
+        bsh[a] = rec->b[a];
+        omask[a] = bsh[a] >= 32 ? 0xffffffffu : (1u << bsh[a]) - 1u;
+        shifts[a] = s;
+        s += bsh[a];
+        Nn[a] = rec->N[a];
+        mgm[a] = rec->mg_m[a];
+        mgl[a] = rec->mg_l[a];
+      }
+    }
+    const bool q32 = rec->fast_body != 1;  // every bin index < 2^31 (fast bodies 2 and 3)
+    const uint32_t sb = rec->sumb;
+    const uint64_t idx_base = P.out_offsets ? P.out_offsets[blk] : blk * (uint64_t)P.bs;
+    const uint32_t offbad = q32 ? warp_particles<D, F64, true>(P, sm, blk, idx_base, lane, wpre, pbit, so, wo, sb, lo,
+                                                               w, bsh, shifts, Nn, mgm, mgl, omask)
+                                : warp_particles<D, F64, false>(P, sm, blk, idx_base, lane, wpre, pbit, so, wo, sb,
+                                                                lo, w, bsh, shifts, Nn, mgm, mgl, omask);
+    if (__any_sync(kFull, offbad != 0) && lane == 0) report_decode_error(R, blk, 1u << 14);
+    __syncwarp();
+  }
+}
+
+// The CTA decoder over K4a's list of the remaining blocks (persistent CTAs).
+template <int D, bool F64, bool PRES>
+__global__ void __launch_bounds__(kThreads, GPZB_K4_MINB) k_decode_list(const DecParams P, const uint32_t* list) {
+  __shared__ DecSmem sm;
+  const uint32_t cnt = *reinterpret_cast<volatile const uint32_t*>(&P.res->wide_count);
+  for (uint32_t i = blockIdx.x; i < cnt; i += gridDim.x) {
+    const uint64_t blk = list[i];
+    const DecRec* rec = P.rec + blk;
+    if (!PRES && rec->fast_body) decode_fast<D, F64>(P, sm, blk, rec);
+    else decode_general<D, F64, PRES>(P, sm, blk, rec);
+    __syncthreads();
+  }
+}
+
+}  // namespace gpzb

@@ -2,7 +2,7 @@
 # A/B: bench the default build and every build/*.so variant (compress/decompress GB/s only)
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
-for lib in paper_2508_10305_b200/_gpzb.so build/*.so; do
+for lib in paper_2508_10305_b200/_gpzb.so $(ls build/*.so 2>/dev/null); do
   echo "== $lib" >> gpurun_out/ab.txt
   GPZB_LIB=$PWD/$lib timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu $AB_ARGS 2>&1 | python -c "
 import json,sys
