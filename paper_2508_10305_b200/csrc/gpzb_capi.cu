@@ -149,8 +149,11 @@ void launch_decode(const DecParams& P, bool pres, cudaStream_t s) {
                            (int)kWarpDecSmemBytes);
       attr = true;
     }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_warp<D, F64>, 32 * kWarpDecWarps,
+                                                  kWarpDecSmemBytes);
     const unsigned wgrid = (unsigned)std::min<uint64_t>((P.nblocks + kWarpDecWarps - 1) / kWarpDecWarps,
-                                                        (uint64_t)sm_count() * 3);
+                                                        (uint64_t)sm_count() * std::max(per_sm, 1));
     k_decode_warp<D, F64><<<wgrid, 32 * kWarpDecWarps, kWarpDecSmemBytes, s>>>(P);
     k_decode_list<D, F64, false><<<lgrid, kThreads, 0, s>>>(P, P.list);
   }

@@ -47,7 +47,7 @@ struct __align__(16) DecRec {
   uint8_t pn_all;     // Π N >= 2^64 (every id in range)
   uint8_t fast_body;  // 32-bit decode body applies (see k_decode); 2: with the midpoint table; 3: 32-bit q
   uint16_t lut1, lut2;  // fast_body 2: table offsets of axes 1 and 2 (axis 0 starts at 0)
-  uint16_t lut_n;       // fast_body 2: table entries (Σ N_a 2^b_a)
+  uint16_t lut_n;       // table entries Σ N_a 2^b_a when <= kLutEntries (else 0); lut1/lut2 valid then
 };
 static_assert(sizeof(DecRec) == 128, "DecRec layout");
 
@@ -234,9 +234,9 @@ __global__ void __launch_bounds__(256) k_decode_plan(const DecParams P) {
       if (a == 2) rec.lut2 = (uint16_t)tot;
       tot += (uint64_t)rec.N[a] << rec.b[a];
     }
-    if (tot <= (uint64_t)kLutEntries / (F64 ? 2 : 1) && U <= GPZB_LUT_UMAX) {
+    if (tot <= (uint64_t)kLutEntries / (F64 ? 2 : 1)) rec.lut_n = (uint16_t)tot;  // table offsets valid
+    if (rec.lut_n && U <= GPZB_LUT_UMAX) {
       rec.fast_body = 2;
-      rec.lut_n = (uint16_t)tot;
     } else {
       bool q31 = true;
 #pragma unroll

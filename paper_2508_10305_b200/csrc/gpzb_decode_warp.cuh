@@ -19,10 +19,22 @@
 namespace gpzb {
 
 constexpr int kWinBytes = 4096;            // payload window per warp
-constexpr int kWarpDecWarps = 8;           // warps per CTA
+#ifndef GPZB_K4W_WARPS
+#define GPZB_K4W_WARPS 8
+#endif
+constexpr int kWarpDecWarps = GPZB_K4W_WARPS;  // warps per CTA
+#ifndef GPZB_K4W_MINB
+#define GPZB_K4W_MINB 3
+#endif
+#ifndef GPZB_K4W_LUT_UMAX
+#define GPZB_K4W_LUT_UMAX 256  // <= kWarpLutBase
+#endif
+// blocks with U <= GPZB_K4W_LUT_UMAX runs keep a midpoint table in the unused
+// tail of `uniq` (words 256..1023: 768 f32 / 384 f64 entries)
+constexpr int kWarpLutBase = 256, kWarpLutWords = kMaxBs - kWarpLutBase;
 struct WarpDecSmem {
   uint32_t win[kWinBytes / 4 + 8];
-  uint32_t uniq[kMaxBs];
+  __align__(16) uint32_t uniq[kMaxBs];     // run ids, or packed 10-bit table bases per axis + the table
   uint32_t rstart[kMaxBs / 32];
 };
 constexpr size_t kWarpDecSmemBytes = sizeof(WarpDecSmem) * kWarpDecWarps;
@@ -30,7 +42,7 @@ constexpr size_t kWarpDecSmemBytes = sizeof(WarpDecSmem) * kWarpDecWarps;
 // The particle phase of K4w: 8 chunks of 128 positions, four consecutive
 // per lane (one 16-byte store per axis and chunk).  Q32: every bin index
 // < 2^31, so the 2^51 magic midpoint comes from one 32-bit word.
-template <int D, bool F64, bool Q32>
+template <int D, bool F64, bool Q32, bool LUT>
 __device__ __forceinline__ uint32_t warp_particles(const DecParams& P, const WarpDecSmem& sm, uint64_t blk,
                                                    uint64_t idx_base, int lane, uint32_t wpre, uint32_t pbit,
                                                    uint32_t so, uint32_t wo, uint32_t sb, const double (&lo)[D],
@@ -69,6 +81,15 @@ __device__ __forceinline__ uint32_t warp_particles(const DecParams& P, const War
       const uint32_t run = base + __popc(word & (0xffffffffu >> (31 - b))) - 1;
       const uint32_t off = offs[k];
       if (sb < 32) offbad |= off >> sb;  // quantizer.py:264-265
+      if constexpr (LUT) {
+        // the run's table bases (bin seg_a << b_a of each axis) + this particle's offsets
+        const uint32_t pk = sm.uniq[run];
+        const T* tab = reinterpret_cast<const T*>(sm.uniq + kWarpLutBase);
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+          vals[a][k] = tab[((pk >> (10 * a)) & 0x3ffu) + ((off >> shifts[a]) & omask[a])];
+        continue;
+      }
       uint32_t rest = sm.uniq[run];
 #pragma unroll
       for (int a = 0; a < D; ++a) {
@@ -115,7 +136,7 @@ __device__ __forceinline__ uint32_t warp_particles(const DecParams& P, const War
 }
 
 template <int D, bool F64>
-__global__ void __launch_bounds__(32 * kWarpDecWarps, 3) k_decode_warp(const DecParams P) {
+__global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_warp(const DecParams P) {
   using T = typename std::conditional<F64, double, float>::type;
   extern __shared__ __align__(16) unsigned char dsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -163,6 +184,17 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, 3) k_decode_warp(const Dec
       const uint32_t used = cnt * w, nb = (used + 7) >> 3;
       if (w && cnt && (used & 7) && (pb[st + nb - 1] >> (used & 7))) fl |= 1u << lane;
     }
+    const bool wlut = U <= GPZB_K4W_LUT_UMAX && rec->lut_n != 0 && rec->lut_n <= (F64 ? kWarpLutWords / 2 : kWarpLutWords);
+    if (wlut) {  // every bin's midpoint, RN_T(lo + RN(RN(q + 0.5) w)) (quantizer.py:132-139)
+      T* tab = reinterpret_cast<T*>(sm.uniq + kWarpLutBase);
+      const uint32_t nt = rec->lut_n, l1 = rec->lut1, l2 = rec->lut2;
+      for (uint32_t i = lane; i < nt; i += 32) {
+        const int a = (D > 2 && i >= l2) ? 2 : (D > 1 && i >= l1) ? 1 : 0;
+        const uint32_t q = i - (a == 0 ? 0u : a == 1 ? l1 : l2);
+        const double h = __hiloint2double(0x43200000, (int)(2u * q + 1u));
+        tab[i] = (T)__dadd_rn(rec->lo[a], __dmul_rn(__dsub_rn(h, 2251799813685248.0), rec->w[a]));
+      }
+    }
     // ---- runs: lane l owns runs [l*RPL, (l+1)*RPL)
     const uint32_t RPL = (U + 31) >> 5;
     const uint32_t r0 = lane * RPL, r1 = min(U, r0 + RPL);
@@ -195,7 +227,25 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, 3) k_decode_warp(const Dec
         if (r > 0 && u <= prev) fl |= 1u << 3;  // pipeline.py:116-117
         if (cn < 1) fl |= 1u << 4;              // pipeline.py:118-119
         if (u >= rec->PN) fl |= 1u << 13;       // quantizer.py:262-263
-        sm.uniq[r] = (uint32_t)u;
+        if (wlut) {
+          uint32_t rest = (uint32_t)u, pk = 0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            uint32_t sa;
+            if (a + 1 < D) {
+              const uint32_t qd = magic_div(rest, rec->mg_m[a], rec->mg_l[a]);
+              sa = rest - qd * rec->N[a];
+              rest = qd;
+            } else {
+              sa = rest;
+            }
+            const uint32_t lb = a == 0 ? 0u : a == 1 ? (uint32_t)rec->lut1 : (uint32_t)rec->lut2;
+            pk |= ((lb + (sa << rec->b[a])) & 0x3ffu) << (10 * a);
+          }
+          sm.uniq[r] = pk;
+        } else {
+          sm.uniq[r] = (uint32_t)u;
+        }
         if (cex < (uint32_t)kMaxBs) red_or_shared(&sm.rstart[cex >> 5], 1u << (cex & 31));
         cex += cn;
         prev = u;
@@ -239,10 +289,13 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, 3) k_decode_warp(const Dec
     const bool q32 = rec->fast_body != 1;  // every bin index < 2^31 (fast bodies 2 and 3)
     const uint32_t sb = rec->sumb;
     const uint64_t idx_base = P.out_offsets ? P.out_offsets[blk] : blk * (uint64_t)P.bs;
-    const uint32_t offbad = q32 ? warp_particles<D, F64, true>(P, sm, blk, idx_base, lane, wpre, pbit, so, wo, sb, lo,
-                                                               w, bsh, shifts, Nn, mgm, mgl, omask)
-                                : warp_particles<D, F64, false>(P, sm, blk, idx_base, lane, wpre, pbit, so, wo, sb,
-                                                                lo, w, bsh, shifts, Nn, mgm, mgl, omask);
+    const uint32_t offbad =
+        wlut  ? warp_particles<D, F64, true, true>(P, sm, blk, idx_base, lane, wpre, pbit, so, wo, sb, lo, w, bsh,
+                                                   shifts, Nn, mgm, mgl, omask)
+        : q32 ? warp_particles<D, F64, true, false>(P, sm, blk, idx_base, lane, wpre, pbit, so, wo, sb, lo, w, bsh,
+                                                    shifts, Nn, mgm, mgl, omask)
+              : warp_particles<D, F64, false, false>(P, sm, blk, idx_base, lane, wpre, pbit, so, wo, sb, lo, w,
+                                                     bsh, shifts, Nn, mgm, mgl, omask);
     if (__any_sync(kFull, offbad != 0) && lane == 0) report_decode_error(R, blk, 1u << 14);
     __syncwarp();
   }
