@@ -200,9 +200,14 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
     const uint32_t r0 = lane * RPL, r1 = min(U, r0 + RPL);
     unsigned long long dsum = 0;
     uint32_t csum = 0;
+    // narrow streams: keep each run's (delta, count) from this pass in uniq[r]
+    const bool keep = wd <= 16 && wc <= 16;
     for (uint32_t r = r0; r < r1; ++r) {
-      dsum += get_bits32(sm.win, pbit + 8 * sd + r * wd, wd);
-      csum += get_bits32(sm.win, pbit + 8 * sc + r * wc, wc);
+      const uint32_t dl = get_bits32(sm.win, pbit + 8 * sd + r * wd, wd);
+      const uint32_t cn = get_bits32(sm.win, pbit + 8 * sc + r * wc, wc);
+      dsum += dl;
+      csum += cn;
+      if (keep) sm.uniq[r] = dl | (cn << 16);
     }
     // packed warp scan (Σ deltas < 2^42 in the low 43 bits; run lengths,
     // clamped per lane at 1025, above them: a valid block sums to 1024)
@@ -221,8 +226,15 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
       uint64_t prev = ex & kDMask;
       uint32_t cex = (uint32_t)(ex >> kDBits);
       for (uint32_t r = r0; r < r1; ++r) {
-        const uint32_t dl = get_bits32(sm.win, pbit + 8 * sd + r * wd, wd);
-        const uint32_t cn = get_bits32(sm.win, pbit + 8 * sc + r * wc, wc);
+        uint32_t dl, cn;
+        if (keep) {
+          const uint32_t v = sm.uniq[r];
+          dl = v & 0xffffu;
+          cn = v >> 16;
+        } else {
+          dl = get_bits32(sm.win, pbit + 8 * sd + r * wd, wd);
+          cn = get_bits32(sm.win, pbit + 8 * sc + r * wc, wc);
+        }
         const uint64_t u = prev + dl;
         if (r > 0 && u <= prev) fl |= 1u << 3;  // pipeline.py:116-117
         if (cn < 1) fl |= 1u << 4;              // pipeline.py:118-119
