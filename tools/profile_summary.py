@@ -64,7 +64,7 @@ def kernel_summary(path):
         "dram_read_bytes": rd,
         "dram_write_bytes": wr,
         "dram_bytes_per_launch": rd + wr,
-        "dram_throughput_pct_of_peak": _num(d.get("dram__throughput.avg.pct_of_peak_sustained_elapsed", "0") or 0),
+        "dram_throughput_pct_of_peak": _num(d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "0") or 0),
         "warp_instructions": _num(d["smsp__inst_executed.sum"]),
         "issue_active_pct": _num(d["smsp__issue_active.avg.pct_of_peak_sustained_active"]),
         "warps_active_pct": _num(d["sm__warps_active.avg.pct_of_peak_sustained_active"]),
