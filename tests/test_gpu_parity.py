@@ -216,3 +216,41 @@ def test_large_sampled_block_parity():
         for a in range(3):
             assert np.array_equal(rec.axes[a][sl].cpu().numpy(), dec[a]), f"decode block {i}"
     del host_c
+
+
+@pytest.mark.parametrize("kind", ["clusters", "velocity"])
+def test_bitflips_on_warp_decoded_blocks(kind):
+    """Full 1024-particle blocks take the warp decoder (K4w); the golden bit-flip
+    container above is too small for it.  Seeded single-bit flips over the
+    table and the payloads (every bit of each block's first 64 payload bytes +
+    random ones): error class and "block i" prefix, or the reconstruction,
+    must equal the oracle's (pinned to the reference)."""
+    rng = np.random.default_rng(7 if kind == "clusters" else 8)
+    if kind == "clusters":
+        axes = O.gen_clusters(4096, dims=3, seed=31)
+    else:  # offsets present: bulk motion + per-particle spread
+        bulk = rng.normal(0, 0.3, size=(4, 3))
+        axes = [(np.repeat(bulk[:, a], 1024) + rng.normal(0, 0.05, 4096)).astype(np.float32) for a in range(3)]
+    blob = O.compress(axes, O.Config(1e-3))
+    assert gz.compress(gz.Dataset.from_axes(axes), gz.CompressConfig(1e-3)) == blob
+    h, table, _ = O.read_container(blob)
+    base = 46 + 8 * (h.blocks + 1)
+    positions = set()
+    for i in range(h.blocks):
+        s = base + int(table[i])
+        positions.update(range(s, min(s + 64, base + int(table[i + 1]))))
+    positions.update(rng.integers(46, len(blob), 600).tolist())
+    bad = []
+    for pos in sorted(positions):
+        for bit in range(8):
+            c = bytearray(blob)
+            c[pos] ^= 1 << bit
+            ds, err = _outcome(lambda: gz.decompress(bytes(c)))
+            try:
+                want = ("ok", sha(*O.decompress(bytes(c))))
+            except O.OracleError as exc:
+                want = (type(exc).__name__, error_prefix(str(exc)))
+            got = ("ok", sha(*ds.axes)) if err is None else err
+            if got != want:
+                bad.append((pos, bit, got, want))
+    assert not bad, f"{len(bad)} mismatches, first: {bad[:5]}"
