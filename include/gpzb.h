@@ -131,18 +131,28 @@ int gpzb_encode_plan_async(const void* const* axes, int dims, int precision, uin
  * blocks need (0 when every block takes the fast path). */
 int gpzb_encode_side_bytes(void* ws, uint64_t ws_bytes, void* stream, uint64_t* side_bytes);
 
-/* K2w (general blocks, into `side`) + K2 (fast blocks, decoupled look-back,
- * container assembly), enqueued.  Writes the full container (global header,
- * offset table, payloads) into `out` (capacity from gpzb_compress_bound).
+/* Synchronise and read K1.5's routing: side-buffer bytes for the general
+ * encoder, and how many narrow blocks go to the CTA encoder (K2) and to the
+ * warp encoder (K2p, offset-free blocks).  The counts size the K2 launches. */
+int gpzb_encode_plan_counts(void* ws, uint64_t ws_bytes, void* stream, uint64_t* side_bytes,
+                            uint64_t* cta_blocks, uint64_t* warp_blocks);
+
+/* K2w (general blocks, into `side`) + K2 / K2p (narrow blocks into staging
+ * slots) + K3 (look-back scan of the payload lengths, offset table, payload
+ * moves), enqueued.  Writes the full container (global header, offset
+ * table, payloads) into `out` (capacity from gpzb_compress_bound).
  *   table_base / header_count / header_blocks: sharding hooks — table entries
  *   are written as table_base + local prefix, and the global header (written
  *   when write_header != 0) names header_count particles in header_blocks
- *   blocks.  Single-GPU callers pass 0, count, ceil(count/bs), 1. */
+ *   blocks.  Single-GPU callers pass 0, count, ceil(count/bs), 1.
+ *   cta_blocks / warp_blocks: from gpzb_encode_plan_counts (UINT64_MAX for
+ *   both: unknown, every encoder is launched over all blocks). */
 int gpzb_encode_async(const void* const* axes, int dims, int precision, uint64_t count, double eb,
                       int eb_mode, uint32_t block_size, uint32_t target_segs_per_axis,
                       int preserve_order, void* ws, uint64_t ws_bytes, uint8_t* side,
                       uint64_t side_bytes, uint8_t* out, uint64_t out_cap, uint64_t table_base,
-                      uint64_t header_count, uint64_t header_blocks, int write_header, void* stream);
+                      uint64_t header_count, uint64_t header_blocks, int write_header,
+                      uint64_t cta_blocks, uint64_t warp_blocks, void* stream);
 
 /* Synchronise `stream` and read the result record of the last encode. */
 int gpzb_compress_result(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t block_size,

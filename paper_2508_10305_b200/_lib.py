@@ -68,8 +68,10 @@ SIGNATURES = {
     "gpzb_encode_plan_async": (_I32, [ctypes.POINTER(_VP), _I32, _I32, _U64, _D, _I32, _U32, _U32, _I32, _VP,
                                       _U64, _VP]),
     "gpzb_encode_side_bytes": (_I32, [_VP, _U64, _VP, ctypes.POINTER(_U64)]),
+    "gpzb_encode_plan_counts": (_I32, [_VP, _U64, _VP, ctypes.POINTER(_U64), ctypes.POINTER(_U64),
+                                       ctypes.POINTER(_U64)]),
     "gpzb_encode_async": (_I32, [ctypes.POINTER(_VP), _I32, _I32, _U64, _D, _I32, _U32, _U32, _I32, _VP, _U64,
-                                 _VP, _U64, _VP, _U64, _U64, _U64, _U64, _I32, _VP]),
+                                 _VP, _U64, _VP, _U64, _U64, _U64, _U64, _I32, _U64, _U64, _VP]),
     "gpzb_compress_result": (_I32, [_VP, _U64, _U64, _U32, _VP, _RES]),
     "gpzb_compress": (_I32, [ctypes.POINTER(_VP), _I32, _I32, _U64, _D, _I32, _U32, _U32, _I32, _VP, _U64, _VP,
                              _U64, _VP, _RES]),

@@ -11,6 +11,7 @@
 #include "gpzb_decode_warp.cuh"
 #include "gpzb_encode.cuh"
 #include "gpzb_encode_narrow.cuh"
+#include "gpzb_encode_warp.cuh"
 #include "gpzb_encode_wide.cuh"
 #include "gpzb_metrics.cuh"
 
@@ -26,7 +27,7 @@ constexpr uint64_t kAlign = 256;
 inline uint64_t align_up(uint64_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
 
 struct EncLayout {
-  uint64_t status, tstat, bounds, rec, list, staging, total;
+  uint64_t status, tstat, bounds, rec, list, ctalist, staging, total;
 };
 
 inline uint64_t nblocks_of(uint64_t count, uint32_t bs) { return bs ? (count + bs - 1) / bs : 0; }
@@ -38,7 +39,8 @@ EncLayout enc_layout(uint64_t nblocks, int dims, int prec) {
   L.bounds = align_up(L.tstat + 8 * ((nblocks + kScanTile - 1) / kScanTile));
   L.rec = align_up(L.bounds + nblocks * 2ull * dims * (prec ? 8 : 4));
   L.list = align_up(L.rec + nblocks * sizeof(BlkRec));
-  L.staging = align_up(L.list + 4 * nblocks);
+  L.ctalist = align_up(L.list + 4 * nblocks);
+  L.staging = align_up(L.ctalist + 4 * nblocks);
   L.total = align_up(L.staging + (uint64_t)kSlotBytes * nblocks);
   return L;
 }
@@ -110,13 +112,37 @@ void launch_geometry(const EncParams& P, cudaStream_t s) {
 }
 
 template <int D, bool F64>
-void launch_encode(const EncParams& P, bool wide, cudaStream_t s) {
+void launch_encode(const EncParams& P, bool wide, uint64_t cta_blocks, uint64_t warp_blocks, cudaStream_t s) {
   if (wide) {
     const unsigned grid = (unsigned)std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * 4);
     if (P.preserve) k_encode_wide<D, F64, true><<<grid, kThreads, 0, s>>>(P);
     else k_encode_wide<D, F64, false><<<grid, kThreads, 0, s>>>(P);
   }
-  k_encode<D, F64><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
+  // K2 (CTA encoder): launch-order blocks when no block went to the warp
+  // encoder, else exactly the listed blocks; K2p (warp encoder) when any
+  // block is offset-free (counts from gpzb_encode_plan_counts; ~0 = unknown)
+  const bool known = cta_blocks != ~0ull && warp_blocks != ~0ull;
+  if (!known || cta_blocks > 0) {
+    EncParams Q = P;
+    Q.cta_mode = (known && warp_blocks == 0) ? 0 : 1;
+    const uint64_t grid = Q.cta_mode ? (known ? cta_blocks : P.nblocks) : P.nblocks;
+    if (!known) Q.cta_mode = 2;  // grid over all blocks, entries past the count exit
+    k_encode<D, F64><<<(unsigned)grid, kThreads, 0, s>>>(Q);
+  }
+  if (!known || warp_blocks > 0) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_encode_warp<D, F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kWarpEncSmemBytes);
+      attr = true;
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_encode_warp<D, F64>, 32 * kWarpEncWarps,
+                                                  kWarpEncSmemBytes);
+    const unsigned wgrid = (unsigned)std::min<uint64_t>((P.nblocks + kWarpEncWarps - 1) / kWarpEncWarps,
+                                                        (uint64_t)sm_count() * std::max(per_sm, 1));
+    k_encode_warp<D, F64><<<wgrid, 32 * kWarpEncWarps, kWarpEncSmemBytes, s>>>(P);
+  }
   // K3: scan of the payload lengths, offset table, payload moves
   CompactParams C;
   C.sizes = P.status;
@@ -130,6 +156,15 @@ void launch_encode(const EncParams& P, bool wide, cudaStream_t s) {
   C.side = P.side;
   C.rec = P.rec;
   C.payload = P.payload;
+  C.header = P.header;
+  C.dims = D;
+  C.f64 = F64 ? 1 : 0;
+  C.preserve = P.preserve;
+  C.eb_mode_code = P.eb_mode_code;
+  C.eb = P.eb;
+  C.bs = P.bs;
+  C.header_count = P.header_count;
+  C.header_blocks = P.header_blocks;
   k_scan_sizes<<<(unsigned)((P.nblocks + kScanTile - 1) / kScanTile), kScanThreads, 0, s>>>(C);
   k_copy_payloads<<<(unsigned)((P.nblocks + kCopyWarps - 1) / kCopyWarps), 32 * kCopyWarps, 0, s>>>(C);
 }
@@ -224,6 +259,7 @@ EncParams make_enc(const void* const* axes, int dims, int prec, uint64_t count, 
   P.bounds = static_cast<uint8_t*>(ws) + L.bounds;
   P.rec = reinterpret_cast<BlkRec*>(static_cast<uint8_t*>(ws) + L.rec);
   P.wide_list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + L.list);
+  P.cta_list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + L.ctalist);
   return P;
 }
 
@@ -373,10 +409,24 @@ int gpzb_encode_side_bytes(void* ws, uint64_t ws_bytes, void* stream, uint64_t* 
   return cuda_status(e);
 }
 
+int gpzb_encode_plan_counts(void* ws, uint64_t ws_bytes, void* stream, uint64_t* side_bytes,
+                            uint64_t* cta_blocks, uint64_t* warp_blocks) {
+  if (ws_bytes < sizeof(DevResult)) return GPZB_INVALID_ARGUMENT;
+  DevResult R;
+  cudaError_t e = cudaMemcpyAsync(&R, ws, sizeof(R), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e);
+  *side_bytes = R.side_bytes;
+  *cta_blocks = R.cta_count;
+  *warp_blocks = R.warp_count;
+  return GPZB_OK;
+}
+
 int gpzb_encode_async(const void* const* axes, int dims, int prec, uint64_t count, double eb, int eb_mode,
                       uint32_t bs, uint32_t target, int pres, void* ws, uint64_t ws_bytes, uint8_t* side,
                       uint64_t side_bytes, uint8_t* out, uint64_t out_cap, uint64_t table_base,
-                      uint64_t header_count, uint64_t header_blocks, int write_header, void* stream) {
+                      uint64_t header_count, uint64_t header_blocks, int write_header, uint64_t cta_blocks,
+                      uint64_t warp_blocks, void* stream) {
   int st = check_args(dims, prec, bs);
   if (st) return st;
   if (target == 0 || (target & (target - 1))) return GPZB_INVALID_ARGUMENT;
@@ -400,7 +450,7 @@ int gpzb_encode_async(const void* const* axes, int dims, int prec, uint64_t coun
   P.table_base = table_base;
   P.header_count = header_count;
   P.header_blocks = header_blocks;
-  DISPATCH_DP(dims, prec, launch_encode, P, side_bytes > 0, (cudaStream_t)stream);
+  DISPATCH_DP(dims, prec, launch_encode, P, side_bytes > 0, cta_blocks, warp_blocks, (cudaStream_t)stream);
   return cuda_status(cudaGetLastError());
 }
 
@@ -464,8 +514,8 @@ int gpzb_compress(const void* const* axes, int dims, int prec, uint64_t count, d
   st = gpzb_workspace_reset_async(ws, ws_bytes, count, bs, stream);
   if (!st) st = gpzb_range_async(axes, dims, prec, count, bs, ws, ws_bytes, stream);
   if (!st) st = gpzb_encode_plan_async(axes, dims, prec, count, eb, eb_mode, bs, target, pres, ws, ws_bytes, stream);
-  uint64_t side_bytes = 0;
-  if (!st) st = gpzb_encode_side_bytes(ws, ws_bytes, stream, &side_bytes);
+  uint64_t side_bytes = 0, cta_blocks = ~0ull, warp_blocks = ~0ull;
+  if (!st) st = gpzb_encode_plan_counts(ws, ws_bytes, stream, &side_bytes, &cta_blocks, &warp_blocks);
   void* side = nullptr;
   if (!st && side_bytes) {  // the one allocation of the convenience wrapper (stream-ordered pool)
     cudaError_t e = cudaMallocAsync(&side, side_bytes, s);
@@ -473,7 +523,8 @@ int gpzb_compress(const void* const* axes, int dims, int prec, uint64_t count, d
   }
   if (!st)
     st = gpzb_encode_async(axes, dims, prec, count, eb, eb_mode, bs, target, pres, ws, ws_bytes,
-                           static_cast<uint8_t*>(side), side_bytes, out, out_cap, 0, count, nb, 1, stream);
+                           static_cast<uint8_t*>(side), side_bytes, out, out_cap, 0, count, nb, 1, cta_blocks,
+                           warp_blocks, stream);
   if (side) cudaFreeAsync(side, s);
   if (st) return res->status = st;
   return gpzb_compress_result(ws, ws_bytes, count, bs, stream, res);

@@ -58,8 +58,10 @@ struct DevResult {
   double eb_abs;
   unsigned long long path_blocks[6];
   unsigned long long side_bytes;    // K1.5: bytes reserved in the side buffer for wide blocks
-  unsigned int wide_count;          // K1.5: number of wide blocks
-  unsigned int pad_;
+  unsigned int wide_count;          // K1.5: number of wide blocks (decode: K4a's CTA-list length)
+  unsigned int cta_count;           // K1.5: narrow blocks for the CTA encoder (its list length)
+  unsigned int warp_count;          // K1.5: blocks for the warp encoder
+  unsigned int pad_[3];
 };
 static_assert(sizeof(DevResult) % 16 == 0, "DevResult alignment");
 

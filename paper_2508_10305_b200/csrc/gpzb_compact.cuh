@@ -42,7 +42,29 @@ struct CompactParams {
   const uint8_t* side;        // general blocks: rec.side_off
   const BlkRec* rec;
   uint8_t* payload;           // block 0's payload byte
+  // global header (container.py:211-230), written by tile 0 when non-null
+  uint8_t* header;
+  int dims, f64, preserve, eb_mode_code;
+  double eb;
+  uint32_t bs;
+  uint64_t header_count, header_blocks;
 };
+
+__device__ void write_global_header(const CompactParams& P) {
+  uint8_t* h = P.header;
+  auto put = [](uint8_t* d, uint64_t v, int nb) { for (int i = 0; i < nb; ++i) d[i] = (uint8_t)(v >> (8 * i)); };
+  h[0] = 'G'; h[1] = 'P'; h[2] = 'Z'; h[3] = '1';
+  put(h + 4, 1, 2);
+  h[6] = (uint8_t)P.dims;
+  h[7] = P.f64 ? 1 : 0;
+  h[8] = P.preserve ? 1 : 0;
+  h[9] = (uint8_t)P.eb_mode_code;
+  put(h + 10, (uint64_t)__double_as_longlong(P.eb), 8);
+  put(h + 18, (uint64_t)__double_as_longlong(P.res->eb_abs), 8);
+  put(h + 26, P.bs, 4);
+  put(h + 30, P.header_count, 8);
+  put(h + 38, P.header_blocks, 8);
+}
 
 // Little-endian u64 at an arbitrary (at least 2-byte aligned when `even`) address.
 __device__ __forceinline__ void put_u64_le(uint8_t* p, uint64_t v, bool even) {
@@ -125,6 +147,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_sizes(const CompactParams
     }
   }
   if (tile == 0 && tid == 0 && P.table0) put_u64_le(P.table0, P.table_base, false);
+  if (tile == 0 && tid == 32 && P.header) write_global_header(P);
 }
 
 // Move `len` payload bytes from a 16-byte aligned slot to dst (any

@@ -43,6 +43,8 @@ struct EncParams {
   int preserve;
   BlkRec* rec;             // per-block geometry records (K1.5)
   uint32_t* wide_list;     // blocks routed to the general encoder
+  uint32_t* cta_list;      // narrow blocks for the CTA encoder (the rest of them go to the warp encoder)
+  int cta_mode;            // 0: CTA i encodes block i (every narrow block is a CTA block); 1: CTA i takes cta_list[i]
   uint8_t* side;           // staging for the general encoder's payloads
   uint8_t* staging;        // narrow payloads: one kSlotBytes slot per block (K3 concatenates)
 };
@@ -347,7 +349,11 @@ struct __align__(16) BlkRec {
 };
 static_assert(sizeof(BlkRec) == 128, "BlkRec layout");
 
-enum : uint8_t { KIND_NARROW = 0, KIND_WIDE = 1, KIND_ERROR = 2 };
+enum : uint8_t { KIND_NARROW = 0, KIND_WIDE = 1, KIND_ERROR = 2, KIND_WARP = 3 };
+
+// Narrow blocks the warp encoder K2p takes: full, vector-loadable, no
+// offset stream (every log2 m == 0) and Π N <= 16384.
+constexpr uint32_t kWarpEncMaxPN = 16384;
 
 // Largest payload a block can produce given its geometry (stream widths are
 // bounded by bitlen(ΠN - 1), bitlen(n), Σb and bitlen(n - 1)).
@@ -412,12 +418,20 @@ __global__ void __launch_bounds__(256) k_geometry(const EncParams P) {
   if (err) {
     rec.kind = KIND_ERROR;
     atomicMax(&R->err_block, err_code(blk, eax, err));
+    P.status[blk] = 0;  // error blocks contribute no bytes
   } else {
     narrow = narrow && PN <= 65536 && sumb <= 32;
     rec.PN = narrow ? (uint32_t)PN : 0u;
     rec.sumb = (uint8_t)sumb;
     if (narrow) {
-      rec.kind = KIND_NARROW;
+      const uint64_t n = min((uint64_t)P.bs, P.count - blk * (uint64_t)P.bs);
+      if (sumb == 0 && PN <= kWarpEncMaxPN && n == (uint64_t)kMaxBs && P.vec && P.cta_list) {
+        rec.kind = KIND_WARP;
+        atomicAdd(&R->warp_count, 1u);
+      } else {
+        rec.kind = KIND_NARROW;
+        if (P.cta_list) P.cta_list[atomicAdd(&R->cta_count, 1u)] = (uint32_t)blk;
+      }
     } else {
       rec.kind = KIND_WIDE;
       const uint32_t n = (uint32_t)min((uint64_t)P.bs, P.count - blk * (uint64_t)P.bs);

@@ -52,24 +52,6 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// Global header (container.py:211-230), by one thread of block 0.
-template <int D, bool F64>
-__device__ void write_global_header(const EncParams& P, double eb_abs) {
-  if (!P.header) return;
-  uint8_t* h = P.header;
-  h[0] = 'G'; h[1] = 'P'; h[2] = 'Z'; h[3] = '1';
-  put_le(h + 4, 1, 2);
-  h[6] = (uint8_t)D;
-  h[7] = F64 ? 1 : 0;
-  h[8] = P.preserve ? 1 : 0;
-  h[9] = (uint8_t)P.eb_mode_code;
-  put_le(h + 10, (uint64_t)__double_as_longlong(P.eb), 8);
-  put_le(h + 18, (uint64_t)__double_as_longlong(eb_abs), 8);
-  put_le(h + 26, P.bs, 4);
-  put_le(h + 30, P.header_count, 8);
-  put_le(h + 38, P.header_blocks, 8);
-}
-
 // Vectorised loads of a full block's 4 particles per thread (16-byte aligned axes).
 template <int D, typename T>
 __device__ __forceinline__ void load_full(const EncParams& P, uint64_t first, int p0, T (&x)[D][kItems]) {
@@ -446,31 +428,24 @@ template <int D, bool F64>
 __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncParams P) {
   __shared__ NarrowSmem sm;
   const int tid = threadIdx.x;
-  DevResult* R = P.res;
-
-  // Blocks in launch order (CTAs are dispatched in blockIdx order, which is
-  // what the look-back's forward progress needs; no ticket atomic).
   using T = typename std::conditional<F64, double, float>::type;
-  const uint64_t blk = blockIdx.x;
-  const uint64_t first = blk * (uint64_t)P.bs;
-  const int n = (int)min((uint64_t)P.bs, P.count - first);
-  const bool full = n == kMaxBs && P.vec;
-  T x[D][kItems];
-  if (full) load_full<D, T>(P, first, tid * kItems, x);  // in flight while the record is staged
-  if (tid < 8) reinterpret_cast<uint4*>(&sm.rec)[tid] = reinterpret_cast<const uint4*>(P.rec + blk)[tid];
-  __syncthreads();
-  const BlkRec* rec = &sm.rec;
-  const uint32_t kind = rec->kind;
-  if (blk == 0 && tid == 32) write_global_header<D, F64>(P, R->eb_abs);
-
-  if (kind != KIND_NARROW) {
-    // general blocks were staged by K2w; error blocks contribute no bytes
-    if (tid == 0) P.status[blk] = (kind == KIND_WIDE) ? rec->side_len : 0ull;
-    return;
+  // one block per CTA: block i in launch order when every narrow block is
+  // ours, else entry i of K1.5's list (the grid is sized to it)
+  {
+    if (P.cta_mode == 2 && blockIdx.x >= *reinterpret_cast<volatile const uint32_t*>(&P.res->cta_count)) return;
+    const uint64_t blk = P.cta_mode ? (uint64_t)P.cta_list[blockIdx.x] : (uint64_t)blockIdx.x;
+    const uint64_t first = blk * (uint64_t)P.bs;
+    const int n = (int)min((uint64_t)P.bs, P.count - first);
+    const bool full = n == kMaxBs && P.vec;
+    T x[D][kItems];
+    if (full) load_full<D, T>(P, first, tid * kItems, x);  // in flight while the record is staged
+    if (tid < 8) reinterpret_cast<uint4*>(&sm.rec)[tid] = reinterpret_cast<const uint4*>(P.rec + blk)[tid];
+    __syncthreads();
+    const BlkRec* rec = &sm.rec;
+    if (rec->kind != KIND_NARROW) return;  // cta_mode 0: general / error blocks are sized elsewhere
+    if (full) narrow_body<D, F64, true>(P, sm, blk, rec, n, x);
+    else narrow_body<D, F64, false>(P, sm, blk, rec, n, x);
   }
-
-  if (full) narrow_body<D, F64, true>(P, sm, blk, rec, n, x);
-  else narrow_body<D, F64, false>(P, sm, blk, rec, n, x);
 }
 
 }  // namespace gpzb

@@ -1,0 +1,237 @@
+// K2p: warp-per-block encoder for offset-free blocks.
+//
+// When every axis has log2 m == 0 (one bin per segment, so the offset stream
+// is empty and the (seg, off) sort is the segment sort alone) and Π N <=
+// 16384, a block's whole state — presence bitmap, word prefixes, run lengths,
+// unique ids, the payload stage — fits ~10 KB, so one warp can own a block:
+// 32 particles per lane, warp scans and __syncwarp instead of CTA barriers.
+// Same steps and bytes as the CTA encoder (gpzb_encode_narrow.cuh):
+//
+//   quantize (certified reciprocal, quantizer.py:142-191) -> seg per particle
+//   presence bitmap over [0, Π N) -> word prefixes -> rank of each particle's
+//   segment; RED.ADD per rank -> run lengths; unique ids by rank
+//   (rle_encode(sort(seg)), codec.py:53-79, blocksort.py:17-28)
+//   widths by OR (codec.width_for), payload length -> sizes[blk]
+//   header + delta + count streams bit-packed in shared memory
+//   (container.serialize_block, container.py:102-121), 16-byte stores into
+//   the block's staging slot for K3.
+#pragma once
+
+#include "gpzb_encode_narrow.cuh"
+
+namespace gpzb {
+
+#ifndef GPZB_K2P_WARPS
+#define GPZB_K2P_WARPS 8
+#endif
+constexpr int kWarpEncWarps = GPZB_K2P_WARPS;
+// payload <= 74 + 1024 * (14 + 11) / 8 + 2 = 3,276 bytes (widths <= bitlen(16383), bitlen(1024))
+constexpr int kWarpStageWords = 832;
+struct WarpEncSmem {
+  __align__(16) uint32_t bm[kWarpStageWords];  // presence bitmap (<= 512 words), then the payload stage
+  uint16_t wp[kWarpEncMaxPN / 32];             // set bits before each bitmap word
+  __align__(16) uint32_t cnt[kMaxBs];          // run length per segment rank
+  uint16_t uniqp[kMaxBs + 2];                  // [0] = 0 sentinel, [r + 1] = unique id r
+};
+constexpr size_t kWarpEncSmemBytes = sizeof(WarpEncSmem) * kWarpEncWarps;
+
+template <int D, bool F64>
+__global__ void __launch_bounds__(32 * kWarpEncWarps) k_encode_warp(const EncParams P) {
+  using T = typename std::conditional<F64, double, float>::type;
+  constexpr int S = F64 ? 8 : 4;
+  constexpr uint32_t H = 8 + D * (2 * S + 5) + 3;  // block header bytes (container.py:62-67)
+  constexpr int VE = 16 / S;                        // coordinates per 16-byte load
+  extern __shared__ __align__(16) unsigned char esm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpEncSmem& sm = reinterpret_cast<WarpEncSmem*>(esm)[wid];
+  DevResult* R = P.res;
+
+  for (uint64_t blk = (uint64_t)blockIdx.x * kWarpEncWarps + wid; blk < P.nblocks;
+       blk += (uint64_t)gridDim.x * kWarpEncWarps) {
+    const BlkRec* rec = P.rec + blk;
+    if (rec->kind != KIND_WARP) continue;  // warp-uniform
+    const uint64_t first = blk * (uint64_t)P.bs;
+    const uint32_t PN = rec->PN;
+    const uint32_t nw = (PN + 31) >> 5;
+    // ---- zero the bitmap and the run counters
+    for (uint32_t w = lane; w < (nw + 3) >> 2; w += 32) reinterpret_cast<uint4*>(sm.bm)[w] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int j = 0; j < kMaxBs / 128; ++j) reinterpret_cast<uint4*>(sm.cnt)[j * 32 + lane] = make_uint4(0, 0, 0, 0);
+    if (lane == 0) sm.uniqp[0] = 0;
+    double lo[D], rinv[D];
+    uint32_t Nst[D];
+    {
+      uint32_t st = 1;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        lo[a] = rec->lo[a];
+        rinv[a] = rec->rinv[a];
+        Nst[a] = st;
+        st *= rec->N[a];
+      }
+    }
+    __syncwarp();
+    // ---- quantize: chunk c, lane l -> particles c*128 + 4l .. +3 (b == 0: q_a is the segment digit)
+    uint32_t segpk[kMaxBs / 64];  // 32 segment ids, two 16-bit ids per register
+#pragma unroll
+    for (int c = 0; c < kMaxBs / 128; ++c) {
+      const uint32_t p0 = c * 128 + 4 * lane;
+      T x[D][4];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const uint4* base = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(P.axes[a]) + first + p0);
+#pragma unroll
+        for (int v = 0; v < 4 / VE; ++v) {
+          const uint4 u = __ldcs(base + v);
+          const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+          for (int j = 0; j < VE; ++j) x[a][v * VE + j] = e[j];
+        }
+      }
+      uint32_t seg[4] = {0, 0, 0, 0};
+      bool bad = false;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          // certified reciprocal quantizer (gpzb_common.cuh quantize_coord, mode 0)
+          const double t = __dsub_rn((double)x[a][k], lo[a]);
+          const double r = __dmul_rn(t, rinv[a]);
+          const uint32_t rl = (uint32_t)__double2loint(r), rh = (uint32_t)__double2hiint(r);
+          const uint32_t q = (uint32_t)__double2loint(__dadd_rz(r, 4503599627370496.0));
+          bad |= ((rl + 1u) <= 1u) & (rh != 0u);  // r == 0 (t == 0) is exact
+          seg[k] += q * Nst[a];
+        }
+      }
+      if (__any_sync(kFull, bad)) {
+        if (bad) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t so = redo_exact<D, T>(x[0][k], D > 1 ? x[D > 1 ? 1 : 0][k] : T(0),
+                                                 D > 2 ? x[D > 2 ? 2 : 0][k] : T(0), rec);
+            seg[k] = (uint32_t)(so >> 32);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) red_or_shared(&sm.bm[seg[k] >> 5], 1u << (seg[k] & 31));
+      segpk[2 * c] = seg[0] | (seg[1] << 16);
+      segpk[2 * c + 1] = seg[2] | (seg[3] << 16);
+    }
+    __syncwarp();
+    // ---- word prefixes: lane l owns bitmap words [16l, 16l + 16)
+    uint32_t U;
+    {
+      uint32_t local = 0;
+      const uint32_t w0 = 16 * lane;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (w0 + 4 * j < nw) {
+          const uint4 q = reinterpret_cast<const uint4*>(sm.bm)[4 * lane + j];
+          local += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+        }
+      }
+      uint32_t incl = local;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      U = __shfl_sync(kFull, incl, 31);
+      uint32_t run = incl - local;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (w0 + 4 * j < nw) {
+          const uint4 q = reinterpret_cast<const uint4*>(sm.bm)[4 * lane + j];
+          const uint32_t a = run, b = a + __popc(q.x), c = b + __popc(q.y), d = c + __popc(q.z);
+          reinterpret_cast<uint2*>(sm.wp)[4 * lane + j] = make_uint2(a | (b << 16), c | (d << 16));
+          run = d + __popc(q.w);
+        }
+      }
+    }
+    __syncwarp();
+    // ---- ranks -> run lengths and unique ids
+#pragma unroll
+    for (int i = 0; i < kMaxBs / 64; ++i) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t sg = (segpk[i] >> (16 * h)) & 0xffffu;
+        const uint32_t w = sg >> 5;
+        const uint32_t rk = (uint32_t)sm.wp[w] + __popc(sm.bm[w] & ((1u << (sg & 31)) - 1u));
+        atomicAdd(&sm.cnt[rk], 1u);  // no return value used: RED
+        sm.uniqp[rk + 1] = (uint16_t)sg;
+      }
+    }
+    __syncwarp();
+    // ---- widths (width_for == bit length of the OR) and the payload length
+    uint32_t c_or = 0, d_or = 0;
+    for (uint32_t r = lane; r < U; r += 32) {
+      c_or |= sm.cnt[r];
+      d_or |= (uint32_t)sm.uniqp[r + 1] - (uint32_t)sm.uniqp[r];
+    }
+    c_or = __reduce_or_sync(kFull, c_or);
+    d_or = __reduce_or_sync(kFull, d_or);
+    const uint32_t w_cnt = bitlen32(c_or), w_del = bitlen32(d_or);
+    const uint32_t Ld = (U * w_del + 7) >> 3, Lc = (U * w_cnt + 7) >> 3;
+    const uint32_t L = H + Ld + Lc;
+    if (lane == 0) {
+      P.status[blk] = L;  // payload length for the K3 scan
+      atomicAdd(&R->path_blocks[0], 1ull);
+    }
+    // ---- bit-pack into the stage (the bitmap is dead now)
+    uint32_t* st = sm.bm;
+    const uint32_t nquads = (L + 15) >> 4;
+    for (uint32_t w = lane; w < nquads; w += 32) reinterpret_cast<uint4*>(st)[w] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+    {
+      // block header fields, one per lane (container.serialize_block, container.py:107-121)
+      const int f = lane;
+      uint32_t bpos = 0;
+      uint64_t val = 0;
+      bool act = true;
+      if (f == 0) { bpos = 0; val = (uint32_t)kMaxBs; }
+      else if (f == 1) { bpos = 4; val = U; }
+      else if (f < 2 + 4 * D) {
+        const int a = (f - 2) >> 2, which = (f - 2) & 3;
+        const uint32_t ab = 8 + a * (2 * S + 5);
+        const T* bnd = reinterpret_cast<const T*>(P.bounds) + blk * 2 * D;
+        if (which < 2) {
+          bpos = ab + which * S;
+          const T v = bnd[2 * a + which];
+          if constexpr (F64) val = (uint64_t)__double_as_longlong(v);
+          else val = __float_as_uint(v);
+        } else if (which == 2) { bpos = ab + 2 * S; val = 0; }  // log2 m == 0
+        else { bpos = ab + 2 * S + 1; val = rec->N[a]; }
+      } else if (f < 2 + 4 * D + 3) {
+        const int wi = f - 2 - 4 * D;
+        bpos = 8 + D * (2 * S + 5) + wi;
+        val = wi == 0 ? w_del : wi == 1 ? w_cnt : 0u;  // w_off == 0
+      } else {
+        act = false;
+      }
+      if (act) or_bits(st, 8ull * bpos, val);
+    }
+    {
+      const uint64_t bd = 8ull * H, bc = bd + 8ull * Ld;
+      for (uint32_t r0 = 4 * lane; r0 < U; r0 += 128) {
+        uint64_t dv = 0, cv = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t r = r0 + j;
+          if (r < U) {
+            dv |= (uint64_t)((uint32_t)sm.uniqp[r + 1] - (uint32_t)sm.uniqp[r]) << (j * w_del);
+            cv |= (uint64_t)sm.cnt[r] << (j * w_cnt);
+          }
+        }
+        if (w_del) or_bits(st, bd + (uint64_t)r0 * w_del, dv);
+        if (w_cnt) or_bits(st, bc + (uint64_t)r0 * w_cnt, cv);
+      }
+    }
+    __syncwarp();
+    uint4* slot = reinterpret_cast<uint4*>(P.staging + blk * (uint64_t)kSlotBytes);
+    for (uint32_t w = lane; w < nquads; w += 32) __stcg(slot + w, reinterpret_cast<const uint4*>(st)[w]);
+    __syncwarp();  // the next block reuses the shared state
+  }
+}
+
+}  // namespace gpzb

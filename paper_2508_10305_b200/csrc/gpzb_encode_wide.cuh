@@ -405,7 +405,10 @@ __global__ void __launch_bounds__(kThreads) k_encode_wide(const EncParams P) {
   // ---- 10. stage -> side buffer (16B aligned, whole chunks)
   for (uint32_t c = tid; c < nch; c += kThreads)
     reinterpret_cast<uint4*>(dst)[c] = reinterpret_cast<const uint4*>(st)[c];
-  if (tid == 0) rec->side_len = (uint32_t)L;
+  if (tid == 0) {
+    rec->side_len = (uint32_t)L;
+    P.status[blk] = L;  // payload length for the K3 scan
+  }
   }
 }
 

@@ -149,13 +149,14 @@ def compress_device(ds, cfg: CompressConfig, *, timing=None) -> torch.Tensor:
             timing.setdefault("range", []).append((e0, ev()))
         _check(lib.gpzb_encode_plan_async(ptrs, dims, prec, count, eb, mode, bs, t, pres, ws.data_ptr(),
                                           ws.numel(), stream))
-        side_bytes = ctypes.c_uint64()
-        _check(lib.gpzb_encode_side_bytes(ws.data_ptr(), ws.numel(), stream, ctypes.byref(side_bytes)))
+        side_bytes, cta_b, warp_b = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib.gpzb_encode_plan_counts(ws.data_ptr(), ws.numel(), stream, ctypes.byref(side_bytes),
+                                            ctypes.byref(cta_b), ctypes.byref(warp_b)))
         side = torch.empty(max(side_bytes.value, 16), dtype=torch.uint8, device=axes[0].device)
         e0 = ev() if timing is not None else None
         _check(lib.gpzb_encode_async(ptrs, dims, prec, count, eb, mode, bs, t, pres, ws.data_ptr(), ws.numel(),
                                      side.data_ptr(), side_bytes.value, out.data_ptr(), bound.value, 0, count, nb,
-                                     1, stream))
+                                     1, cta_b.value, warp_b.value, stream))
         if timing is not None:
             timing.setdefault("encode", []).append((e0, ev()))
         st = lib.gpzb_compress_result(ws.data_ptr(), ws.numel(), count, bs, stream, ctypes.byref(res))

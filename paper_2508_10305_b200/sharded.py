@@ -121,13 +121,13 @@ class _CudaHooks:
             self._check(lib.gpzb_range_async(self.ptrs, ds.dims, ds.precision.value, ds.count, cfg.block_size,
                                              self.ws.data_ptr(), self.ws.numel(), self._stream()))
         self._check(lib.gpzb_encode_plan_async(*args, self._stream()))
-        side_bytes = ctypes.c_uint64()
-        self._check(lib.gpzb_encode_side_bytes(self.ws.data_ptr(), self.ws.numel(), self._stream(),
-                                               ctypes.byref(side_bytes)))
+        side_bytes, cta_b, warp_b = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        self._check(lib.gpzb_encode_plan_counts(self.ws.data_ptr(), self.ws.numel(), self._stream(),
+                                                ctypes.byref(side_bytes), ctypes.byref(cta_b), ctypes.byref(warp_b)))
         side = torch.empty(max(side_bytes.value, 16), dtype=torch.uint8, device=self.axes[0].device)
         e0 = self._ev() if self.timing is not None else None
         self._check(lib.gpzb_encode_async(*args, side.data_ptr(), side_bytes.value, out.data_ptr(), bound.value,
-                                          0, ds.count, nb, 1, self._stream()))
+                                          0, ds.count, nb, 1, cta_b.value, warp_b.value, self._stream()))
         if self.timing is not None:
             self.timing.setdefault("encode", []).append((e0, self._ev()))
         res = _lib.Result()
