@@ -22,7 +22,10 @@
 namespace gpzb {
 
 #ifndef GPZB_K2P_WARPS
-#define GPZB_K2P_WARPS 8
+#define GPZB_K2P_WARPS 4
+#endif
+#ifndef GPZB_K2P_MINB
+#define GPZB_K2P_MINB 5
 #endif
 constexpr int kWarpEncWarps = GPZB_K2P_WARPS;
 // payload <= 74 + 1024 * (14 + 11) / 8 + 2 = 3,276 bytes (widths <= bitlen(16383), bitlen(1024))
@@ -36,7 +39,7 @@ struct WarpEncSmem {
 constexpr size_t kWarpEncSmemBytes = sizeof(WarpEncSmem) * kWarpEncWarps;
 
 template <int D, bool F64>
-__global__ void __launch_bounds__(32 * kWarpEncWarps) k_encode_warp(const EncParams P) {
+__global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_warp(const EncParams P) {
   using T = typename std::conditional<F64, double, float>::type;
   constexpr int S = F64 ? 8 : 4;
   constexpr uint32_t H = 8 + D * (2 * S + 5) + 3;  // block header bytes (container.py:62-67)
