@@ -28,6 +28,8 @@ __all__ = [
     "compress",
     "decompress",
     "compress_device",
+    "compress_batch_device",
+    "decompress_batch_device",
     "decompress_device",
     "iter_block_slices",
     "iter_decompressed_blocks",
@@ -52,13 +54,15 @@ def _stream() -> int:
 _WS: dict = {}
 
 
-def _workspace(nbytes: int) -> torch.Tensor:
-    """Per-device scratch, grown on demand (the library never allocates)."""
+def _workspace(nbytes: int, slot: int = 0) -> torch.Tensor:
+    """Per-device scratch, grown on demand (the library never allocates);
+    one buffer per concurrent slot (compress_batch_device)."""
     dev = _device()
-    buf = _WS.get(dev.index)
+    key = (dev.index, slot)
+    buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=dev)
-        _WS[dev.index] = buf
+        _WS[key] = buf
     return buf
 
 
@@ -111,58 +115,131 @@ def _device_axes(ds: Dataset) -> list:
     return out
 
 
+class _Job:
+    """One dataset's compression in flight (the phases of compress_device)."""
+
+    __slots__ = ("axes", "ptrs", "count", "dims", "prec", "bs", "t", "pres", "eb", "mode", "ws", "out", "bound",
+                 "nb", "res", "stream", "timing")
+
+
+def _ev():
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
+def _compress_begin(ds, cfg: CompressConfig, slot: int, timing) -> _Job:
+    """Allocate and enqueue the workspace reset, K1 and K1.5 (no host sync)."""
+    j = _Job()
+    ds = _as_dataset(ds)
+    j.axes = _device_axes(ds)
+    j.count, j.dims, j.prec = ds.count, ds.dims, ds.precision.value
+    j.bs, j.t, j.pres = cfg.block_size, cfg.target_segs_per_axis, int(cfg.preserve_order)
+    j.eb, j.mode = float(cfg.error_bound), cfg.eb_mode.value
+    j.timing = timing
+    ws_bytes = ctypes.c_uint64()
+    _check(lib.gpzb_compress_workspace(j.count, j.dims, j.prec, j.bs, ctypes.byref(ws_bytes)))
+    bound = ctypes.c_uint64()
+    _check(lib.gpzb_compress_bound(j.count, j.dims, j.prec, j.bs, j.t, j.pres, ctypes.byref(bound)))
+    j.bound = bound.value
+    j.ws = _workspace(ws_bytes.value, slot)
+    j.out = torch.empty(j.bound, dtype=torch.uint8, device=j.axes[0].device)
+    j.ptrs = _lib.ptr_array([a.data_ptr() for a in j.axes])
+    j.res = _lib.Result()
+    j.stream = _stream()
+    j.nb = (j.count + j.bs - 1) // j.bs
+    if j.count == 0:
+        return j
+    _check(lib.gpzb_workspace_reset_async(j.ws.data_ptr(), j.ws.numel(), j.count, j.bs, j.stream))
+    e0 = _ev() if timing is not None else None
+    _check(lib.gpzb_range_async(j.ptrs, j.dims, j.prec, j.count, j.bs, j.ws.data_ptr(), j.ws.numel(), j.stream))
+    if timing is not None:
+        timing.setdefault("range", []).append((e0, _ev()))
+    _check(lib.gpzb_encode_plan_async(j.ptrs, j.dims, j.prec, j.count, j.eb, j.mode, j.bs, j.t, j.pres,
+                                      j.ws.data_ptr(), j.ws.numel(), j.stream))
+    return j
+
+
+def _compress_encode(j: _Job) -> None:
+    """Read K1.5's routing (one sync of the job's stream) and enqueue K2 + K3."""
+    if j.count == 0:
+        return
+    side_bytes, cta_b, warp_b = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    _check(lib.gpzb_encode_plan_counts(j.ws.data_ptr(), j.ws.numel(), j.stream, ctypes.byref(side_bytes),
+                                        ctypes.byref(cta_b), ctypes.byref(warp_b)))
+    side = torch.empty(max(side_bytes.value, 16), dtype=torch.uint8, device=j.axes[0].device)
+    e0 = _ev() if j.timing is not None else None
+    _check(lib.gpzb_encode_async(j.ptrs, j.dims, j.prec, j.count, j.eb, j.mode, j.bs, j.t, j.pres, j.ws.data_ptr(),
+                                 j.ws.numel(), side.data_ptr(), side_bytes.value, j.out.data_ptr(), j.bound, 0,
+                                 j.count, j.nb, 1, cta_b.value, warp_b.value, j.stream))
+    if j.timing is not None:
+        j.timing.setdefault("encode", []).append((e0, _ev()))
+
+
+def _compress_finish(j: _Job) -> torch.Tensor:
+    """Read the result record (one sync) and map errors."""
+    if j.count == 0:
+        st = lib.gpzb_compress(j.ptrs, j.dims, j.prec, j.count, j.eb, j.mode, j.bs, j.t, j.pres, j.ws.data_ptr(),
+                               j.ws.numel(), j.out.data_ptr(), j.bound, j.stream, ctypes.byref(j.res))
+    else:
+        st = lib.gpzb_compress_result(j.ws.data_ptr(), j.ws.numel(), j.count, j.bs, j.stream, ctypes.byref(j.res))
+    _check(st, j.res)
+    compress_device.last_result = j.res
+    return j.out[: j.res.out_len]
+
+
 def compress_device(ds, cfg: CompressConfig, *, timing=None) -> torch.Tensor:
     """Container bytes as a CUDA uint8 tensor (a view of the output buffer).
 
     ``timing``: optional dict; when given, CUDA events are recorded on the
-    current stream around the range kernel (K1) and the encode kernel (K2)
-    and appended to ``timing["range"]`` / ``timing["encode"]`` as pairs.
+    current stream around the range kernel (K1) and the encode call (K2 +
+    K3) and appended to ``timing["range"]`` / ``timing["encode"]`` as pairs.
     """
-    ds = _as_dataset(ds)
-    axes = _device_axes(ds)
-    count, dims, prec = ds.count, ds.dims, ds.precision.value
-    bs, t, pres = cfg.block_size, cfg.target_segs_per_axis, int(cfg.preserve_order)
-    ws_bytes = ctypes.c_uint64()
-    _check(lib.gpzb_compress_workspace(count, dims, prec, bs, ctypes.byref(ws_bytes)))
-    bound = ctypes.c_uint64()
-    _check(lib.gpzb_compress_bound(count, dims, prec, bs, t, pres, ctypes.byref(bound)))
-    ws = _workspace(ws_bytes.value)
-    out = torch.empty(bound.value, dtype=torch.uint8, device=axes[0].device)
-    ptrs = _lib.ptr_array([a.data_ptr() for a in axes])
-    res = _lib.Result()
-    stream = _stream()
-    eb, mode = float(cfg.error_bound), cfg.eb_mode.value
-    if count == 0:
-        st = lib.gpzb_compress(ptrs, dims, prec, count, eb, mode, bs, t, pres, ws.data_ptr(), ws.numel(),
-                               out.data_ptr(), bound.value, stream, ctypes.byref(res))
-    else:
-        def ev():
-            e = torch.cuda.Event(enable_timing=True)
-            e.record()
-            return e
+    j = _compress_begin(ds, cfg, 0, timing)
+    _compress_encode(j)
+    return _compress_finish(j)
 
-        nb = (count + bs - 1) // bs
-        _check(lib.gpzb_workspace_reset_async(ws.data_ptr(), ws.numel(), count, bs, stream))
-        e0 = ev() if timing is not None else None
-        _check(lib.gpzb_range_async(ptrs, dims, prec, count, bs, ws.data_ptr(), ws.numel(), stream))
-        if timing is not None:
-            timing.setdefault("range", []).append((e0, ev()))
-        _check(lib.gpzb_encode_plan_async(ptrs, dims, prec, count, eb, mode, bs, t, pres, ws.data_ptr(),
-                                          ws.numel(), stream))
-        side_bytes, cta_b, warp_b = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
-        _check(lib.gpzb_encode_plan_counts(ws.data_ptr(), ws.numel(), stream, ctypes.byref(side_bytes),
-                                            ctypes.byref(cta_b), ctypes.byref(warp_b)))
-        side = torch.empty(max(side_bytes.value, 16), dtype=torch.uint8, device=axes[0].device)
-        e0 = ev() if timing is not None else None
-        _check(lib.gpzb_encode_async(ptrs, dims, prec, count, eb, mode, bs, t, pres, ws.data_ptr(), ws.numel(),
-                                     side.data_ptr(), side_bytes.value, out.data_ptr(), bound.value, 0, count, nb,
-                                     1, cta_b.value, warp_b.value, stream))
-        if timing is not None:
-            timing.setdefault("encode", []).append((e0, ev()))
-        st = lib.gpzb_compress_result(ws.data_ptr(), ws.numel(), count, bs, stream, ctypes.byref(res))
-    _check(st, res)
-    compress_device.last_result = res
-    return out[: res.out_len]
+
+_STREAMS: dict = {}
+
+
+def _side_stream(i: int) -> torch.cuda.Stream:
+    """Stream i of the batched calls: earlier datasets get higher priority, so
+    the first range pass finishes first and its encoder starts while the next
+    range pass still streams (a pipeline instead of two halves contending)."""
+    dev = _device()
+    key = (dev.index, i)
+    if key not in _STREAMS:
+        lo, hi = torch.cuda.Stream.priority_range()  # (lowest, highest); higher priority = smaller number
+        _STREAMS[key] = torch.cuda.Stream(device=dev, priority=max(hi, min(lo, hi + i)))
+    return _STREAMS[key]
+
+
+def compress_batch_device(datasets, cfg: CompressConfig, *, timing=None) -> list:
+    """Compress several datasets (e.g. the position and velocity fields of one
+    snapshot) with one CUDA stream and workspace each, so the HBM-bound range
+    pass (K1) of one overlaps the compute-bound encoder (K2) of another.
+    Returns the containers in order; each is byte-identical to compress_device."""
+    cur = torch.cuda.current_stream()
+    start = torch.cuda.Event()
+    start.record(cur)
+    jobs = []
+    for i, ds in enumerate(datasets):
+        s = _side_stream(i)
+        s.wait_event(start)
+        with torch.cuda.stream(s):
+            jobs.append(_compress_begin(ds, cfg, i, timing))
+    for i, j in enumerate(jobs):
+        with torch.cuda.stream(_side_stream(i)):
+            _compress_encode(j)
+    outs = []
+    for i, j in enumerate(jobs):
+        s = _side_stream(i)
+        with torch.cuda.stream(s):
+            outs.append(_compress_finish(j))
+        cur.wait_stream(s)
+        outs[-1].record_stream(cur)
+    return outs
 
 
 _PINNED: dict = {}
@@ -267,7 +344,8 @@ def _to_device_bytes(data) -> tuple[torch.Tensor, _lib.Header]:
     return t, h
 
 
-def _decode(t: torch.Tensor, h: _lib.Header, offsets=None, capacity=None, timing=None):
+def _decode_launch(t: torch.Tensor, h: _lib.Header, offsets=None, capacity=None, timing=None, slot: int = 0):
+    """Enqueue K4a + K4w + the list decoder; returns what _decode_result needs."""
     prec = Precision(h.precision)
     dev = t.device
     if capacity is None:
@@ -275,23 +353,54 @@ def _decode(t: torch.Tensor, h: _lib.Header, offsets=None, capacity=None, timing
     outs = [torch.empty(max(capacity, 1), dtype=prec.torch_dtype, device=dev) for _ in range(h.dims)]
     ws_bytes = ctypes.c_uint64()
     _check(lib.gpzb_decompress_workspace(ctypes.byref(h), ctypes.byref(ws_bytes)))
-    ws = _workspace(ws_bytes.value)
-    res = _lib.Result()
+    ws = _workspace(ws_bytes.value, slot)
     stream = _stream()
-    e0 = None
-    if timing is not None:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e0.record()
+    e0 = _ev() if timing is not None else None
     _check(lib.gpzb_decompress_async(t.data_ptr(), t.numel(), ctypes.byref(h),
                                      _lib.ptr_array([o.data_ptr() for o in outs]), capacity,
                                      offsets.data_ptr() if offsets is not None else None, ws.data_ptr(),
                                      ws.numel(), stream))
     if timing is not None:
-        e1 = torch.cuda.Event(enable_timing=True)
-        e1.record()
-        timing.setdefault("decode", []).append((e0, e1))
-    lib.gpzb_decompress_result(ws.data_ptr(), ws.numel(), ctypes.byref(h), stream, ctypes.byref(res))
+        timing.setdefault("decode", []).append((e0, _ev()))
+    return outs, ws, h, capacity
+
+
+def _decode_result(launched):
+    outs, ws, h, capacity = launched
+    res = _lib.Result()
+    lib.gpzb_decompress_result(ws.data_ptr(), ws.numel(), ctypes.byref(h), _stream(), ctypes.byref(res))
     return outs, res, capacity
+
+
+def _decode(t: torch.Tensor, h: _lib.Header, offsets=None, capacity=None, timing=None):
+    return _decode_result(_decode_launch(t, h, offsets, capacity, timing))
+
+
+def decompress_batch_device(containers, *, timing=None) -> list:
+    """Decode several containers with one CUDA stream and workspace each
+    (overlapping their kernels); returns Datasets of CUDA tensors in order."""
+    cur = torch.cuda.current_stream()
+    start = torch.cuda.Event()
+    start.record(cur)
+    launched = []
+    for i, data in enumerate(containers):
+        s = _side_stream(i)
+        s.wait_event(start)
+        with torch.cuda.stream(s):
+            t, h = _to_device_bytes(data)
+            launched.append(_decode_launch(t, h, timing=timing, slot=i))
+    out = []
+    for i, L in enumerate(launched):
+        s = _side_stream(i)
+        with torch.cuda.stream(s):
+            outs, res, _ = _decode_result(L)
+            _check(res.status, res)
+        cur.wait_stream(s)
+        for o in outs:
+            o.record_stream(cur)
+        n = L[2].particle_count
+        out.append(Dataset(axes=tuple(o[:n] for o in outs), precision=Precision(L[2].precision)))
+    return out
 
 
 def decompress_device(data, workers: int = 1, *, header=None, timing=None) -> Dataset:

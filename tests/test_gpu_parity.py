@@ -254,3 +254,18 @@ def test_bitflips_on_warp_decoded_blocks(kind):
             if got != want:
                 bad.append((pos, bit, got, want))
     assert not bad, f"{len(bad)} mismatches, first: {bad[:5]}"
+
+
+def test_batched_calls_match_single_calls():
+    """compress_batch_device / decompress_batch_device (one stream + workspace
+    per dataset) give the bytes and values of the one-at-a-time calls."""
+    sets = [O.gen_clusters(300_000, dims=3, seed=s) for s in (1, 2)] + [O.gen_uniform(70_001, dims=2, seed=3)]
+    cfg = gz.CompressConfig(error_bound=1e-3)
+    dss = [gz.Dataset.from_axes([torch.from_numpy(a).cuda() for a in axes]) for axes in sets]
+    batch = gz.compress_batch_device(dss, cfg)
+    for ds, c in zip(dss, batch):
+        assert torch.equal(c, gz.compress_device(ds, cfg))
+    recs = gz.decompress_batch_device(batch)
+    for c, r in zip(batch, recs):
+        want = gz.decompress_device(c)
+        assert all(torch.equal(x, y) for x, y in zip(r.axes, want.axes))
