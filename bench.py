@@ -273,12 +273,16 @@ def main():
     torch.cuda.synchronize()
     timing: dict = {}
     tcs, tds = [], []
+    from paper_2508_10305_b200._lib import lib as _gl
+
+    launches0 = _gl.gpzb_kernel_launches()
     with Clocks(local) as clk:
         for _ in range(args.steps):
             tc, td, sizes = one_step(timing)
             tcs.append(tc)
             tds.append(td)
     torch.cuda.synchronize()
+    launches = int(_gl.gpzb_kernel_launches() - launches0)
     t_c, t_d = sum(tcs), sum(tds)
     if world > 1:
         import torch.distributed as dist
@@ -368,7 +372,7 @@ def main():
                                        for k, v in (("k_encode", enc_ms), ("k_decode", dec_ms), ("k_range", rng_ms))},
                     "k_range_gbps": local_in / rng_avg / 1e9 if rng_ms else None,
                     "k_encode_ms": enc_avg * 1e3, "k_decode_ms": dec_avg * 1e3},
-        "gpu_launches": len(enc_ms) + len(dec_ms) + len(rng_ms),
+        "gpu_launches": launches,
         "clocks": clk.summary,
     }
     if rank == 0 and not args.no_e2e:

@@ -228,6 +228,10 @@ int gpzb_pair_stats(const void* const* orig, const void* const* rec, int dims, i
 const char* gpzb_reason_message(int reason);
 const char* gpzb_version(void);
 
+/* Kernels this library has launched in the process so far (the bench
+ * reports the difference over its timed region). */
+uint64_t gpzb_kernel_launches(void);
+
 #ifdef __cplusplus
 }
 #endif

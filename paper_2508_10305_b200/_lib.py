@@ -87,6 +87,7 @@ SIGNATURES = {
                                _VP, _U64, _VP, _U64, _VP, ctypes.POINTER(_D), ctypes.POINTER(_U64)]),
     "gpzb_reason_message": (ctypes.c_char_p, [_I32]),
     "gpzb_version": (ctypes.c_char_p, []),
+    "gpzb_kernel_launches": (_U64, []),
 }
 
 

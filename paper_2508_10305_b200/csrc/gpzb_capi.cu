@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 
 #include "gpzb_decode.cuh"
 #include "gpzb_decode_warp.cuh"
@@ -24,6 +25,10 @@ namespace {
 #endif
 
 constexpr uint64_t kAlign = 256;
+
+// Kernel launches issued by this library (process-wide; gpzb_kernel_launches).
+std::atomic<unsigned long long> g_launches{0};
+#define GPZB_COUNT_LAUNCH() g_launches.fetch_add(1, std::memory_order_relaxed)
 inline uint64_t align_up(uint64_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
 
 struct EncLayout {
@@ -98,15 +103,18 @@ template <int D, bool F64>
 void launch_range(const EncParams& P, cudaStream_t s) {
 #ifdef GPZB_K1_CTA
   const uint64_t grid = std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * 8);
+  GPZB_COUNT_LAUNCH();
   k_range<D, typename std::conditional<F64, double, float>::type><<<(unsigned)grid, kThreads, 0, s>>>(P);
 #else
   const uint64_t grid = std::min<uint64_t>((P.nblocks + kWarps - 1) / kWarps, (uint64_t)sm_count() * GPZB_K1_CTAS);
+  GPZB_COUNT_LAUNCH();
   k_range_w<D, typename std::conditional<F64, double, float>::type><<<(unsigned)grid, kThreads, 0, s>>>(P);
 #endif
 }
 
 template <int D, bool F64>
 void launch_geometry(const EncParams& P, cudaStream_t s) {
+  GPZB_COUNT_LAUNCH();
   k_geometry<D, typename std::conditional<F64, double, float>::type>
       <<<(unsigned)((P.nblocks + 255) / 256), 256, 0, s>>>(P);
 }
@@ -115,8 +123,8 @@ template <int D, bool F64>
 void launch_encode(const EncParams& P, bool wide, uint64_t cta_blocks, uint64_t warp_blocks, cudaStream_t s) {
   if (wide) {
     const unsigned grid = (unsigned)std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * 4);
-    if (P.preserve) k_encode_wide<D, F64, true><<<grid, kThreads, 0, s>>>(P);
-    else k_encode_wide<D, F64, false><<<grid, kThreads, 0, s>>>(P);
+    if (P.preserve) { GPZB_COUNT_LAUNCH(); k_encode_wide<D, F64, true><<<grid, kThreads, 0, s>>>(P); }
+    else { GPZB_COUNT_LAUNCH(); k_encode_wide<D, F64, false><<<grid, kThreads, 0, s>>>(P); }
   }
   // K2 (CTA encoder): launch-order blocks when no block went to the warp
   // encoder, else exactly the listed blocks; K2p (warp encoder) when any
@@ -127,6 +135,7 @@ void launch_encode(const EncParams& P, bool wide, uint64_t cta_blocks, uint64_t 
     Q.cta_mode = (known && warp_blocks == 0) ? 0 : 1;
     const uint64_t grid = Q.cta_mode ? (known ? cta_blocks : P.nblocks) : P.nblocks;
     if (!known) Q.cta_mode = 2;  // grid over all blocks, entries past the count exit
+    GPZB_COUNT_LAUNCH();
     k_encode<D, F64><<<(unsigned)grid, kThreads, 0, s>>>(Q);
   }
   if (!known || warp_blocks > 0) {
@@ -141,6 +150,7 @@ void launch_encode(const EncParams& P, bool wide, uint64_t cta_blocks, uint64_t 
                                                   kWarpEncSmemBytes);
     const unsigned wgrid = (unsigned)std::min<uint64_t>((P.nblocks + kWarpEncWarps - 1) / kWarpEncWarps,
                                                         (uint64_t)sm_count() * std::max(per_sm, 1));
+    GPZB_COUNT_LAUNCH();
     k_encode_warp<D, F64><<<wgrid, 32 * kWarpEncWarps, kWarpEncSmemBytes, s>>>(P);
   }
   // K3: scan of the payload lengths, offset table, payload moves
@@ -165,7 +175,9 @@ void launch_encode(const EncParams& P, bool wide, uint64_t cta_blocks, uint64_t 
   C.bs = P.bs;
   C.header_count = P.header_count;
   C.header_blocks = P.header_blocks;
+  GPZB_COUNT_LAUNCH();
   k_scan_sizes<<<(unsigned)((P.nblocks + kScanTile - 1) / kScanTile), kScanThreads, 0, s>>>(C);
+  GPZB_COUNT_LAUNCH();
   k_copy_payloads<<<(unsigned)((P.nblocks + kCopyWarps - 1) / kCopyWarps), 32 * kCopyWarps, 0, s>>>(C);
 }
 
@@ -174,9 +186,12 @@ void launch_decode(const DecParams& P, bool pres, cudaStream_t s) {
   const unsigned pgrid = (unsigned)((P.nblocks + 255) / 256);
   const unsigned lgrid = (unsigned)std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * GPZB_K4_MINB);
   if (pres) {
+    GPZB_COUNT_LAUNCH();
     k_decode_plan<D, F64, true><<<pgrid, 256, 0, s>>>(P);
+    GPZB_COUNT_LAUNCH();
     k_decode_list<D, F64, true><<<lgrid, kThreads, 0, s>>>(P, P.list);
   } else {
+    GPZB_COUNT_LAUNCH();
     k_decode_plan<D, F64, false><<<pgrid, 256, 0, s>>>(P);
     static bool attr = false;
     if (!attr) {
@@ -189,7 +204,9 @@ void launch_decode(const DecParams& P, bool pres, cudaStream_t s) {
                                                   kWarpDecSmemBytes);
     const unsigned wgrid = (unsigned)std::min<uint64_t>((P.nblocks + kWarpDecWarps - 1) / kWarpDecWarps,
                                                         (uint64_t)sm_count() * std::max(per_sm, 1));
+    GPZB_COUNT_LAUNCH();
     k_decode_warp<D, F64><<<wgrid, 32 * kWarpDecWarps, kWarpDecSmemBytes, s>>>(P);
+    GPZB_COUNT_LAUNCH();
     k_decode_list<D, F64, false><<<lgrid, kThreads, 0, s>>>(P, P.list);
   }
 }
@@ -211,6 +228,7 @@ template <int D, bool F64, bool R64>
 void launch_pair_blocks(const PairParams& P, cudaStream_t s) {
   using T = typename std::conditional<F64, double, float>::type;
   using R = typename std::conditional<R64, double, float>::type;
+  GPZB_COUNT_LAUNCH();
   k_pair_blocks<D, T, R><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
 }
 
@@ -218,7 +236,9 @@ template <int D, bool F64, bool R64>
 void launch_pair_stats(const PairParams& P, unsigned grid, cudaStream_t s) {
   using T = typename std::conditional<F64, double, float>::type;
   using R = typename std::conditional<R64, double, float>::type;
+  GPZB_COUNT_LAUNCH();
   k_pair_stats<D, T, R><<<grid, kThreads, 0, s>>>(P);
+  GPZB_COUNT_LAUNCH();
   k_pair_stats_final<D><<<1, 32, 0, s>>>(P, (int)grid);
 }
 
@@ -268,6 +288,8 @@ EncParams make_enc(const void* const* axes, int dims, int prec, uint64_t count, 
 extern "C" {
 
 const char* gpzb_version(void) { return "gpzb 0.1 sm_100a"; }
+
+uint64_t gpzb_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 #ifdef GPZB_DEBUG_STATS
 int gpzb_debug_counters(uint64_t* out, int reset) {
@@ -564,6 +586,7 @@ int gpzb_parse_header(const uint8_t* hb, uint64_t avail, uint64_t len, gpzb_head
 int gpzb_block_counts_async(const uint8_t* c, uint64_t len, const gpzb_header* h, uint64_t* counts, void* stream) {
   if (h->block_count == 0) return GPZB_OK;
   const unsigned grid = (unsigned)((h->block_count + 255) / 256);
+  GPZB_COUNT_LAUNCH();
   k_block_counts<<<grid, 256, 0, (cudaStream_t)stream>>>(c, len, h->table_end, h->payload_len, h->block_count,
                                                           counts);
   return cuda_status(cudaGetLastError());

@@ -8,8 +8,10 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 900 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/bench_ncu.json 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_encode$" -s 2 -c 2 -o gpurun_out/prof_encode -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_encode$" -s 1 -c 1 -o gpurun_out/prof_encode -f \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_encode.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_encode_warp$" -s 1 -c 1 -o gpurun_out/prof_encode_warp -f \
+    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_encode_warp.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_copy_payloads$" -s 2 -c 2 -o gpurun_out/prof_copy -f \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_copy.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_decode_warp$" -s 2 -c 2 -o gpurun_out/prof_decode -f \
