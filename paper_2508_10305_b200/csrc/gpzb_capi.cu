@@ -291,17 +291,7 @@ const char* gpzb_version(void) { return "gpzb 0.1 sm_100a"; }
 
 uint64_t gpzb_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
-#ifdef GPZB_DEBUG_STATS
-int gpzb_debug_counters(uint64_t* out, int reset) {
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, gpzb::g_dbg, 8 * sizeof(uint64_t));
-  if (reset) {
-    uint64_t z[8] = {0};
-    cudaMemcpyToSymbol(gpzb::g_dbg, z, sizeof(z));
-  }
-  return 0;
-}
-#endif
+
 
 const char* gpzb_reason_message(int r) {
   switch (r) {

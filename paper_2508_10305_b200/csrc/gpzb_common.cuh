@@ -69,15 +69,6 @@ __host__ __device__ inline unsigned long long err_code(uint64_t blk, int axis, i
   return ~((blk << 12) | ((uint64_t)(axis & 15) << 8) | (uint64_t)reason);
 }
 
-// Experiment builds (-DGPZB_DEBUG_STATS) count events here; read with
-// gpzb_debug_counters (declared only in the experiment tooling).
-#ifdef GPZB_DEBUG_STATS
-__device__ unsigned long long g_dbg[8];
-#define GPZB_DBG(i, v) atomicAdd(&g_dbg[i], (unsigned long long)(v))
-#else
-#define GPZB_DBG(i, v) ((void)0)
-#endif
-
 // ------------------------------------------------------ ordered encodings
 // u64 whose unsigned order equals the numeric order of the double.
 __device__ __forceinline__ unsigned long long ukey(double v) {
