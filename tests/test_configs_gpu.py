@@ -115,3 +115,46 @@ def test_config3_decompression_sweep_1b():
         print(f"1B clusters rel {eb:g}: CR {ds.nbytes / c.numel():.3f}")
         del c, rec
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("dims,f64,pres,eb", [(3, True, False, 1e-6), (2, False, True, 1e-3), (1, False, False, 1e-5),
+                                             (3, False, True, 1e-4)])
+def test_other_layouts_at_scale(dims, f64, pres, eb):
+    """20M particles: float64 inputs, 1D/2D, preserve_order (rank stream +
+    general encoder/decoder) — sampled blocks against the oracle, the whole
+    reconstruction under the bound (K5), and order preservation."""
+    n = 20_000_000
+    g = torch.Generator(device="cuda").manual_seed(77 + dims)
+    dt = torch.float64 if f64 else torch.float32
+    c = torch.rand(2048, dims, generator=g, device="cuda", dtype=torch.float64)
+    assign = torch.arange(n, device="cuda") * 2048 // n
+    axes = [(c[assign, a] + 0.003 * torch.randn(n, generator=g, device="cuda", dtype=torch.float64)).to(dt)
+            for a in range(dims)]
+    del assign
+    cfg = gz.CompressConfig(error_bound=eb, preserve_order=pres)
+    ds = gz.Dataset.from_axes(axes)
+    cont = gz.compress_device(ds, cfg)
+    rec = gz.decompress_device(cont)
+    nb = (n + 1023) // 1024
+    head = cont[:46].cpu().numpy().tobytes()
+    table = cont[46: 46 + 8 * (nb + 1)].cpu().numpy().view("<u8")
+    pay0 = 46 + 8 * (nb + 1)
+    eb_abs = float(np.frombuffer(head[18:26], "<f8")[0])
+    prec = O.F64 if f64 else O.F32
+    oc = O.Config(eb, block_size=1024, preserve_order=pres)
+    h = O.Header(dims, prec, pres, 1, eb, eb_abs, 1024, n, nb)
+    for i in _picks(nb, 60, seed=dims):
+        sl = slice(i * 1024, min((i + 1) * 1024, n))
+        block = [a[sl].cpu().numpy() for a in axes]
+        want = O.encode_block(block, eb_abs, oc, prec)
+        got = cont[pay0 + int(table[i]): pay0 + int(table[i + 1])].cpu().numpy().tobytes()
+        assert got == want, f"block {i}"
+        dec = O.decode_block(want, h)
+        for a in range(dims):
+            assert np.array_equal(rec.axes[a][sl].cpu().numpy(), dec[a]), f"decode block {i}"
+    if pres:  # particles come back in their original order, each within the bound
+        for a in range(dims):
+            err = (rec.axes[a].double() - axes[a].double()).abs().max().item()
+            assert err <= eb_abs
+    rep = gz.verify_bound(ds, rec, eb_abs, cfg)
+    assert rep.ok and rep.max_err <= eb_abs
