@@ -49,8 +49,10 @@ __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_wa
   WarpEncSmem& sm = reinterpret_cast<WarpEncSmem*>(esm)[wid];
   DevResult* R = P.res;
 
-  for (uint64_t blk = (uint64_t)blockIdx.x * kWarpEncWarps + wid; blk < P.nblocks;
-       blk += (uint64_t)gridDim.x * kWarpEncWarps) {
+  uint4 raw[D][4 / VE];      // 16-byte loads of the chunk being (or about to be) quantized
+  uint64_t raw_blk = ~0ull;  // block whose chunk 0 sits in raw
+  const uint64_t stride = (uint64_t)gridDim.x * kWarpEncWarps;
+  for (uint64_t blk = (uint64_t)blockIdx.x * kWarpEncWarps + wid; blk < P.nblocks; blk += stride) {
     const BlkRec* rec = P.rec + blk;
     if (rec->kind != KIND_WARP) continue;  // warp-uniform
     const uint64_t first = blk * (uint64_t)P.bs;
@@ -76,19 +78,35 @@ __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_wa
     __syncwarp();
     // ---- quantize: chunk c, lane l -> particles c*128 + 4l .. +3 (b == 0: q_a is the segment digit)
     uint32_t segpk[kMaxBs / 64];  // 32 segment ids, two 16-bit ids per register
+    // software pipeline: chunk c + 1's loads are in flight while chunk c
+    // quantizes; chunk 0 was prefetched while the previous block packed
+    if (raw_blk != blk) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const uint4* base = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(P.axes[a]) + first + 4 * lane);
+#pragma unroll
+        for (int v = 0; v < 4 / VE; ++v) raw[a][v] = __ldcs(base + v);
+      }
+    }
 #pragma unroll
     for (int c = 0; c < kMaxBs / 128; ++c) {
-      const uint32_t p0 = c * 128 + 4 * lane;
       T x[D][4];
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        const uint4* base = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(P.axes[a]) + first + p0);
 #pragma unroll
         for (int v = 0; v < 4 / VE; ++v) {
-          const uint4 u = __ldcs(base + v);
-          const T* e = reinterpret_cast<const T*>(&u);
+          const T* e = reinterpret_cast<const T*>(&raw[a][v]);
 #pragma unroll
           for (int j = 0; j < VE; ++j) x[a][v * VE + j] = e[j];
+        }
+      }
+      if (c + 1 < kMaxBs / 128) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const uint4* base = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(P.axes[a]) + first +
+                                                             (c + 1) * 128 + 4 * lane);
+#pragma unroll
+          for (int v = 0; v < 4 / VE; ++v) raw[a][v] = __ldcs(base + v);
         }
       }
       uint32_t seg[4] = {0, 0, 0, 0};
@@ -120,6 +138,18 @@ __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_wa
       for (int k = 0; k < 4; ++k) red_or_shared(&sm.bm[seg[k] >> 5], 1u << (seg[k] & 31));
       segpk[2 * c] = seg[0] | (seg[1] << 16);
       segpk[2 * c + 1] = seg[2] | (seg[3] << 16);
+    }
+    // prefetch the next block's chunk 0 (full blocks: always in bounds)
+    raw_blk = ~0ull;
+    if (blk + stride < P.nblocks && (blk + stride + 1) * (uint64_t)P.bs <= P.count) {
+      raw_blk = blk + stride;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const uint4* base = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(P.axes[a]) +
+                                                           raw_blk * (uint64_t)P.bs + 4 * lane);
+#pragma unroll
+        for (int v = 0; v < 4 / VE; ++v) raw[a][v] = __ldcs(base + v);
+      }
     }
     __syncwarp();
     // ---- word prefixes: lane l owns bitmap words [16l, 16l + 16)
