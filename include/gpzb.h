@@ -72,7 +72,7 @@ typedef struct gpzb_result {
   int64_t count_block;     /* first block whose particle count breaks the boundary math, or -1 */
   uint32_t table_flags;    /* bit0 start!=0, bit1 not nondecreasing, bit2 end!=payload */
   uint32_t pad_;
-  uint64_t path_blocks[6]; /* blocks per sort path (diagnostics) */
+  uint64_t path_blocks[6]; /* reserved (see gpzb_encode_path_counts) */
 } gpzb_result;
 
 typedef struct gpzb_header {   /* GlobalHeader, container.py:84-95 */
@@ -164,6 +164,12 @@ int gpzb_compress(const void* const* axes, int dims, int precision, uint64_t cou
                   int eb_mode, uint32_t block_size, uint32_t target_segs_per_axis,
                   int preserve_order, void* ws, uint64_t ws_bytes, uint8_t* out,
                   uint64_t out_cap, void* stream, gpzb_result* res);
+
+/* Diagnostics: blocks of the last compression in `ws` per offset-order path
+ * (0 no offsets, 1 composite bitmap, 2 in-group compare, 3 LSD, 4 general
+ * encoder, 5 group masks or general with ranks).  Synchronous. */
+int gpzb_encode_path_counts(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t block_size, int dims,
+                            int precision, void* stream, uint64_t* counts);
 
 /* ---- decompression ------------------------------------------------------ */
 

@@ -88,6 +88,7 @@ SIGNATURES = {
     "gpzb_reason_message": (ctypes.c_char_p, [_I32]),
     "gpzb_version": (ctypes.c_char_p, []),
     "gpzb_kernel_launches": (_U64, []),
+    "gpzb_encode_path_counts": (_I32, [_VP, _U64, _U64, _U32, _I32, _I32, _VP, ctypes.POINTER(_U64)]),
 }
 
 

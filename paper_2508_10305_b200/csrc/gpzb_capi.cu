@@ -477,7 +477,6 @@ int gpzb_compress_result(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t b
   const uint64_t nb = nblocks_of(count, bs);
   res->nonfinite_mask = R.nonfinite_mask;
   res->eb_abs = R.eb_abs;
-  memcpy(res->path_blocks, R.path_blocks, sizeof(res->path_blocks));
   if (R.nonfinite_mask) {  // Dataset construction fails before any block (model.py:75-77)
     res->status = GPZB_DOMAIN_ERROR;
     res->reason = R_NONFINITE;
@@ -491,6 +490,26 @@ int gpzb_compress_result(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t b
   }
   res->out_len = GPZB_GLOBAL_HEADER_SIZE + 8 * (nb + 1) + R.total_payload;
   return GPZB_OK;
+}
+
+int gpzb_encode_path_counts(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t bs, int dims, int prec,
+                            void* stream, uint64_t* counts) {
+  if (check_args(dims, prec, bs)) return GPZB_INVALID_ARGUMENT;
+  const uint64_t nb = nblocks_of(count, bs);
+  const EncLayout L = enc_layout(nb, dims, prec);
+  if (ws_bytes < L.total) return GPZB_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* dev = &reinterpret_cast<DevResult*>(ws)->path_blocks[0];
+  cudaError_t e = cudaMemsetAsync(dev, 0, 6 * sizeof(unsigned long long), s);
+  if (e == cudaSuccess && nb) {
+    GPZB_COUNT_LAUNCH();
+    k_path_counts<<<(unsigned)std::min<uint64_t>((nb + 255) / 256, 1024), 256, 0, s>>>(
+        reinterpret_cast<const BlkRec*>(static_cast<uint8_t*>(ws) + L.rec), nb, dev);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(counts, dev, 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return cuda_status(e);
 }
 
 int gpzb_compress(const void* const* axes, int dims, int prec, uint64_t count, double eb, int eb_mode,

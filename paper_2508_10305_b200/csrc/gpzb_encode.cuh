@@ -344,8 +344,9 @@ struct __align__(16) BlkRec {
   uint32_t side_len;  // wide blocks: payload length (written by K2w)
   uint8_t b[3];       // log2(m) per axis
   uint8_t sumb;       // Σ log2(m)
-  uint8_t kind;       // 0 narrow, 1 wide, 2 error
-  uint8_t pad[23];
+  uint8_t kind;       // KIND_* below
+  uint8_t path;       // K2 / K2p / K2w: the offset-order path taken (diagnostics, gpzb_encode_path_counts)
+  uint8_t pad[22];
 };
 static_assert(sizeof(BlkRec) == 128, "BlkRec layout");
 

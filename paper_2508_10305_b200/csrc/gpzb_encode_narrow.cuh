@@ -97,7 +97,6 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
   constexpr int S = F64 ? 8 : 4;
   constexpr uint32_t H = 8 + D * (2 * S + 5) + 3;  // block header bytes (container.py:62-67)
   const int tid = threadIdx.x;
-  DevResult* R = P.res;
   const uint64_t first = blk * (uint64_t)P.bs;
   const int p0 = tid * kItems;
 #define VALID(k) (FULL || p0 + (k) < n)
@@ -352,7 +351,7 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
 
   // ---- 5. bit-pack header + streams into the stage (payload byte 0 = stage byte 0)
   uint32_t* st = sm.u.stage;
-  if (tid == 0) atomicAdd(&R->path_blocks[path], 1ull);
+  if (tid == 0) P.rec[blk].path = (uint8_t)path;  // diagnostics: gpzb_encode_path_counts
   const uint32_t nquads = (L + 15) >> 4;
   for (uint32_t w = tid; w < nquads; w += kThreads) reinterpret_cast<uint4*>(st)[w] = make_uint4(0, 0, 0, 0);
   __syncthreads();

@@ -47,7 +47,6 @@ __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_wa
   extern __shared__ __align__(16) unsigned char esm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpEncSmem& sm = reinterpret_cast<WarpEncSmem*>(esm)[wid];
-  DevResult* R = P.res;
 
   uint4 raw[D][4 / VE];      // 16-byte loads of the chunk being (or about to be) quantized
   uint64_t raw_blk = ~0ull;  // block whose chunk 0 sits in raw
@@ -209,7 +208,7 @@ __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_wa
     const uint32_t L = H + Ld + Lc;
     if (lane == 0) {
       P.status[blk] = L;  // payload length for the K3 scan
-      atomicAdd(&R->path_blocks[0], 1ull);
+      P.rec[blk].path = 0;  // diagnostics: gpzb_encode_path_counts
     }
     // ---- bit-pack into the stage (the bitmap is dead now)
     uint32_t* st = sm.bm;

@@ -345,11 +345,11 @@ __global__ void __launch_bounds__(kThreads) k_encode_wide(const EncParams P) {
     }
   }
 
-  if (tid == 0) atomicAdd(&R->path_blocks[err ? 5 : 4], 1ull);
+  BlkRec* rec = reinterpret_cast<BlkRec*>(P.rec) + blk;
+  if (tid == 0) rec->path = (uint8_t)(err ? 5 : 4);  // diagnostics: gpzb_encode_path_counts
   if (err) continue;  // cannot happen: K1.5 routes error blocks elsewhere
 
   // ---- 9. bit-pack header + streams into the realigned stage
-  BlkRec* rec = reinterpret_cast<BlkRec*>(P.rec) + blk;
   uint8_t* dst = P.side + rec->side_off;  // 16B aligned
   const uint32_t al = 0;
   const uint32_t nbytes = al + (uint32_t)L;

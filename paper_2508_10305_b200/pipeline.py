@@ -185,7 +185,21 @@ def _compress_finish(j: _Job) -> torch.Tensor:
         st = lib.gpzb_compress_result(j.ws.data_ptr(), j.ws.numel(), j.count, j.bs, j.stream, ctypes.byref(j.res))
     _check(st, j.res)
     compress_device.last_result = j.res
+    _LAST.update(ws=j.ws, count=j.count, bs=j.bs, dims=j.dims, prec=j.prec)
     return j.out[: j.res.out_len]
+
+
+_LAST: dict = {}
+
+
+def last_path_counts() -> list:
+    """Diagnostics: blocks per offset-order path of the last compression
+    (include/gpzb.h gpzb_encode_path_counts)."""
+    c = (ctypes.c_uint64 * 6)()
+    w = _LAST
+    _check(lib.gpzb_encode_path_counts(w["ws"].data_ptr(), w["ws"].numel(), w["count"], w["bs"], w["dims"],
+                                       w["prec"], _stream(), c))
+    return list(c)
 
 
 def compress_device(ds, cfg: CompressConfig, *, timing=None) -> torch.Tensor:
