@@ -189,6 +189,18 @@ int gpzb_decompress_async(const uint8_t* container, uint64_t container_len, cons
                           void* const* axes_out, uint64_t out_capacity, const uint64_t* out_offsets,
                           void* ws, uint64_t ws_bytes, void* stream);
 
+/* gpzb_decompress_async over blocks [first_block, last_block) only, so a host
+ * pipeline can decode a container chunk by chunk as its bytes arrive (block
+ * i reads only table entries i, i+1 and its own payload).  reset = 1 starts a
+ * new decode (clears the outcome in ws); later ranges of the same container
+ * pass 0 and accumulate into it, and gpzb_decompress_result then reports
+ * exactly what one gpzb_decompress_async over all blocks would.  Ranges of
+ * one container go on one stream, in any order. */
+int gpzb_decompress_range_async(const uint8_t* container, uint64_t container_len, const gpzb_header* h,
+                                void* const* axes_out, uint64_t out_capacity, const uint64_t* out_offsets,
+                                void* ws, uint64_t ws_bytes, uint64_t first_block, uint64_t last_block,
+                                int reset, void* stream);
+
 /* Synchronise `stream` and classify the decode outcome in the reference's
  * precedence (table checks, first failing block, finiteness, total count). */
 int gpzb_decompress_result(void* ws, uint64_t ws_bytes, const gpzb_header* h, void* stream,

@@ -79,6 +79,8 @@ SIGNATURES = {
     "gpzb_block_counts_async": (_I32, [_VP, _U64, _HDR, _VP, _VP]),
     "gpzb_decompress": (_I32, [_VP, _U64, _HDR, ctypes.POINTER(_VP), _U64, _VP, _VP, _U64, _VP, _RES]),
     "gpzb_decompress_async": (_I32, [_VP, _U64, _HDR, ctypes.POINTER(_VP), _U64, _VP, _VP, _U64, _VP]),
+    "gpzb_decompress_range_async": (_I32, [_VP, _U64, _HDR, ctypes.POINTER(_VP), _U64, _VP, _VP, _U64, _U64, _U64,
+                                           _I32, _VP]),
     "gpzb_decompress_result": (_I32, [_VP, _U64, _HDR, _VP, _RES]),
     "gpzb_pair_workspace": (_I32, [_U64, _I32, ctypes.POINTER(_U64)]),
     "gpzb_pair_blocks": (_I32, [ctypes.POINTER(_VP), ctypes.POINTER(_VP), _I32, _I32, _I32, _U64, _D, _U32, _U32,

@@ -183,8 +183,9 @@ void launch_encode(const EncParams& P, bool wide, uint64_t cta_blocks, uint64_t 
 
 template <int D, bool F64>
 void launch_decode(const DecParams& P, bool pres, cudaStream_t s) {
-  const unsigned pgrid = (unsigned)((P.nblocks + 255) / 256);
-  const unsigned lgrid = (unsigned)std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * GPZB_K4_MINB);
+  const uint64_t nb = P.blk_hi - P.blk_lo;
+  const unsigned pgrid = (unsigned)((nb + 255) / 256);
+  const unsigned lgrid = (unsigned)std::min<uint64_t>(nb, (uint64_t)sm_count() * GPZB_K4_MINB);
   if (pres) {
     GPZB_COUNT_LAUNCH();
     k_decode_plan<D, F64, true><<<pgrid, 256, 0, s>>>(P);
@@ -202,7 +203,7 @@ void launch_decode(const DecParams& P, bool pres, cudaStream_t s) {
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_warp<D, F64>, 32 * kWarpDecWarps,
                                                   kWarpDecSmemBytes);
-    const unsigned wgrid = (unsigned)std::min<uint64_t>((P.nblocks + kWarpDecWarps - 1) / kWarpDecWarps,
+    const unsigned wgrid = (unsigned)std::min<uint64_t>((nb + kWarpDecWarps - 1) / kWarpDecWarps,
                                                         (uint64_t)sm_count() * std::max(per_sm, 1));
     GPZB_COUNT_LAUNCH();
     k_decode_warp<D, F64><<<wgrid, 32 * kWarpDecWarps, kWarpDecSmemBytes, s>>>(P);
@@ -601,14 +602,18 @@ int gpzb_block_counts_async(const uint8_t* c, uint64_t len, const gpzb_header* h
   return cuda_status(cudaGetLastError());
 }
 
-int gpzb_decompress_async(const uint8_t* c, uint64_t len, const gpzb_header* h, void* const* axes_out,
-                          uint64_t out_cap, const uint64_t* out_offsets, void* ws, uint64_t ws_bytes,
-                          void* stream) {
+int gpzb_decompress_range_async(const uint8_t* c, uint64_t len, const gpzb_header* h, void* const* axes_out,
+                                uint64_t out_cap, const uint64_t* out_offsets, void* ws, uint64_t ws_bytes,
+                                uint64_t first_block, uint64_t last_block, int reset, void* stream) {
   if (ws_bytes < sizeof(DevResult)) return GPZB_INVALID_ARGUMENT;
+  if (first_block > last_block || last_block > h->block_count) return GPZB_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(DevResult), s);
+  DevResult* R = reinterpret_cast<DevResult*>(ws);
+  // a new decode clears the whole outcome; a further range only the list count
+  cudaError_t e = reset ? cudaMemsetAsync(R, 0, sizeof(DevResult), s)
+                        : cudaMemsetAsync(&R->wide_count, 0, sizeof(R->wide_count), s);
   if (e != cudaSuccess) return cuda_status(e);
-  if (h->block_count == 0) return GPZB_OK;
+  if (first_block == last_block) return GPZB_OK;
   if (h->block_count > 0x7fffffffull) return GPZB_UNSUPPORTED;
   DecParams P;
   memset(&P, 0, sizeof(P));
@@ -623,13 +628,22 @@ int gpzb_decompress_async(const uint8_t* c, uint64_t len, const gpzb_header* h, 
   for (uint32_t a = 0; a < h->dims; ++a) P.out[a] = axes_out[a];
   P.out_cap = out_cap;
   P.out_offsets = out_offsets;
-  P.res = reinterpret_cast<DevResult*>(ws);
+  P.res = R;
   const uint64_t list_off = align_up(sizeof(DevResult)) + align_up(h->block_count * sizeof(DecRec));
   if (ws_bytes < list_off + 4 * h->block_count) return GPZB_INVALID_ARGUMENT;
   P.rec = reinterpret_cast<DecRec*>(static_cast<uint8_t*>(ws) + align_up(sizeof(DevResult)));
   P.list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + list_off);
+  P.blk_lo = first_block;
+  P.blk_hi = last_block;
   DISPATCH_DP(h->dims, h->precision, launch_decode, P, h->preserve_order != 0, s);
   return cuda_status(cudaGetLastError());
+}
+
+int gpzb_decompress_async(const uint8_t* c, uint64_t len, const gpzb_header* h, void* const* axes_out,
+                          uint64_t out_cap, const uint64_t* out_offsets, void* ws, uint64_t ws_bytes,
+                          void* stream) {
+  return gpzb_decompress_range_async(c, len, h, axes_out, out_cap, out_offsets, ws, ws_bytes, 0,
+                                     h->block_count, 1, stream);
 }
 
 int gpzb_decompress_result(void* ws, uint64_t ws_bytes, const gpzb_header* h, void* stream, gpzb_result* res) {

@@ -64,6 +64,7 @@ struct DecParams {
   DevResult* res;
   DecRec* rec;
   uint32_t* list;          // K4a: blocks for the CTA decoder (count in res->wide_count)
+  uint64_t blk_lo, blk_hi; // this launch decodes blocks [blk_lo, blk_hi) (chunked host pipelines)
 };
 
 constexpr int kDecStageWords = 5120;  // 20 KB payload window (legit blocks <= 19.2 KB)
@@ -92,8 +93,8 @@ __global__ void __launch_bounds__(256) k_decode_plan(const DecParams P) {
   using T = typename std::conditional<F64, double, float>::type;
   constexpr int S = F64 ? 8 : 4;
   constexpr uint32_t HS = 8 + D * (2 * S + 5) + (PRES ? 4 : 3);
-  const uint64_t blk = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (blk >= P.nblocks) return;
+  const uint64_t blk = P.blk_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (blk >= P.blk_hi) return;
   DevResult* R = P.res;
   DecRec rec;
   memset(&rec, 0, sizeof(rec));

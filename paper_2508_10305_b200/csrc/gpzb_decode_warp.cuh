@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
   DevResult* R = P.res;
   const uint8_t* cend = P.c + P.len;
 
-  for (uint64_t blk = (uint64_t)blockIdx.x * kWarpDecWarps + wid; blk < P.nblocks;
+  for (uint64_t blk = P.blk_lo + (uint64_t)blockIdx.x * kWarpDecWarps + wid; blk < P.blk_hi;
        blk += (uint64_t)gridDim.x * kWarpDecWarps) {
     const DecRec* rec = P.rec + blk;
     if (rec->kind != 2) continue;  // warp-uniform

@@ -279,31 +279,44 @@ _MADV_HUGEPAGE = 14
 _POOL = None
 
 
-def _par_memmove(dst: int, src: int, n: int) -> None:
-    """memmove split over host threads (ctypes releases the GIL)."""
+def _pool():
     global _POOL
-    if n < (32 << 20):
-        ctypes.memmove(dst, src, n)
-        return
     if _POOL is None:
         import concurrent.futures
         import os
 
-        _POOL = concurrent.futures.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
-    parts = _POOL._max_workers
-    step = (n + parts - 1) // parts
-    futs = [_POOL.submit(ctypes.memmove, dst + o, src + o, min(step, n - o)) for o in range(0, n, step)]
+        _POOL = concurrent.futures.ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1))
+    return _POOL
+
+
+def _memmove_parts(dst: int, src: int, n: int, futs: list) -> None:
+    """Queue a memmove split over the host threads (ctypes releases the GIL)."""
+    pool = _pool()
+    step = max(4 << 20, (n + pool._max_workers - 1) // pool._max_workers)
+    futs.extend(pool.submit(ctypes.memmove, dst + o, src + o, min(step, n - o)) for o in range(0, n, step))
+
+
+def _par_memmove(dst: int, src: int, n: int) -> None:
+    if n < (32 << 20):
+        ctypes.memmove(dst, src, n)
+        return
+    futs: list = []
+    _memmove_parts(dst, src, n, futs)
     for f in futs:
         f.result()
 
 
+_CHUNK = 64 << 20  # host <-> device pipelining granule
+
+
 def _device_to_bytes(t: torch.Tensor) -> bytes:
-    """A fresh ``bytes`` object holding a device buffer: one D2H into a cached
-    pinned buffer, then a threaded copy into the bytes storage (advised to
-    transparent huge pages, so first-touch faults are 2 MiB, not 4 KiB)."""
+    """A fresh ``bytes`` object holding a device buffer.  The D2H runs in
+    64 MiB chunks into a cached pinned buffer; each chunk is moved into the
+    bytes storage by the host threads as soon as its copy lands, so the PCIe
+    copy and the host copy (and its first-touch page faults, 2 MiB ones:
+    the storage is advised to transparent huge pages) overlap."""
     n = t.numel()
     host = _pinned(n)[:n]
-    host.copy_(t)
     b = _api.PyBytes_FromStringAndSize(None, n)
     addr = ctypes.cast(ctypes.c_char_p(b), ctypes.c_void_p).value
     if _libc is not None and n >= (4 << 20):
@@ -311,7 +324,23 @@ def _device_to_bytes(t: torch.Tensor) -> bytes:
         s0, s1 = (addr + hp - 1) & ~(hp - 1), (addr + n) & ~(hp - 1)
         if s1 > s0:
             _libc.madvise(s0, s1 - s0, _MADV_HUGEPAGE)
-    _par_memmove(addr, host.data_ptr(), n)
+    if n < 2 * _CHUNK:
+        host.copy_(t)
+        _par_memmove(addr, host.data_ptr(), n)
+        return b
+    stream = torch.cuda.current_stream(t.device)
+    evs = []
+    for o in range(0, n, _CHUNK):
+        host[o: o + _CHUNK].copy_(t[o: o + _CHUNK], non_blocking=True)
+        e = torch.cuda.Event()
+        e.record(stream)
+        evs.append((o, min(_CHUNK, n - o), e))
+    futs: list = []
+    for o, m, e in evs:
+        e.synchronize()
+        _memmove_parts(addr + o, host.data_ptr() + o, m, futs)
+    for f in futs:
+        f.result()
     return b
 
 
@@ -350,11 +379,16 @@ def _to_device_bytes(data) -> tuple[torch.Tensor, _lib.Header]:
         return t, parse_header(head, t.numel())
     host = _host_bytes(data)
     h = parse_header(host[: _lib.GLOBAL_HEADER_SIZE].tobytes(), host.size)
-    # threaded copy into the cached pinned buffer, then one H2D at full PCIe rate
-    stage = _pinned(host.size)[: host.size]
-    _par_memmove(stage.data_ptr(), host.ctypes.data, host.size)
-    t = torch.empty(host.size, dtype=torch.uint8, device=_device())
-    t.copy_(stage)
+    # threaded copies into the cached pinned buffer, 64 MiB at a time, each
+    # chunk's H2D queued as soon as it is staged (host and PCIe copies overlap)
+    n = host.size
+    stage = _pinned(n)[:n]
+    t = torch.empty(n, dtype=torch.uint8, device=_device())
+    for o in range(0, n, _CHUNK):
+        m = min(_CHUNK, n - o)
+        _par_memmove(stage.data_ptr() + o, host.ctypes.data + o, m)
+        t[o: o + m].copy_(stage[o: o + m], non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()  # the stage is reused by the next call
     return t, h
 
 
@@ -417,6 +451,105 @@ def decompress_batch_device(containers, *, timing=None) -> list:
     return out
 
 
+_COPY_STREAM: dict = {}
+
+
+def _copy_stream(i: int = 0) -> torch.cuda.Stream:
+    dev = _device()
+    st = _COPY_STREAM.get((dev.index, i))
+    if st is None:
+        st = _COPY_STREAM[(dev.index, i)] = torch.cuda.Stream(device=dev)
+    return st
+
+
+def _streamed_plan(host: np.ndarray, h: _lib.Header):
+    """Block ranges for a chunked decode of a host container, or None when the
+    container is small or its offset table is not well formed (the one-shot
+    path then reports the reference's error for it)."""
+    nb = h.block_count
+    n = host.size
+    if (nb < 2 or h.particle_count == 0 or n < (32 << 20) or h.table_end + h.payload_len != n
+            or h.block_size > _lib.MAX_BLOCK_SIZE):
+        return None
+    tab = host[_lib.GLOBAL_HEADER_SIZE: _lib.GLOBAL_HEADER_SIZE + 8 * (nb + 1)].view("<u8")
+    if int(tab[0]) != 0 or int(tab[-1]) != h.payload_len or bool(np.any(tab[1:] < tab[:-1])):
+        return None
+    # chunks balanced by blocks (the axes' D2H dominates), at least 16 so the
+    # last chunk's copy-out is a small tail, and at most _CHUNK payload bytes each
+    k = max(16, -(-h.payload_len // _CHUNK))
+    cuts = sorted(set(int(c) for c in np.linspace(0, nb, min(k, nb) + 1).round()))
+    return tab, list(zip(cuts[:-1], cuts[1:]))
+
+
+def _decode_streamed(host: np.ndarray, h: _lib.Header, plan, to_host: bool) -> Dataset:
+    """decompress of a host container with the copies pipelined: chunk k's
+    bytes are staged into pinned memory (host threads) and sent while chunk
+    k-1 decodes (gpzb_decompress_range_async) and chunk k-2's particles go
+    back to pinned host memory on a second stream.  The outcome (errors in
+    the reference's precedence) is that of one decode over all blocks."""
+    tab, chunks = plan
+    n = host.size
+    prec = Precision(h.precision)
+    dev = _device()
+    count, bs = h.particle_count, h.block_size
+    capacity = min(count, h.block_count * min(bs, _lib.MAX_BLOCK_SIZE))
+    outs = [torch.empty(capacity, dtype=prec.torch_dtype, device=dev) for _ in range(h.dims)]
+    ptrs = _lib.ptr_array([o.data_ptr() for o in outs])
+    ws_bytes = ctypes.c_uint64()
+    _check(lib.gpzb_decompress_workspace(ctypes.byref(h), ctypes.byref(ws_bytes)))
+    ws = _workspace(ws_bytes.value, 0)
+    stage = _pinned(n)[:n]
+    t = torch.empty(n, dtype=torch.uint8, device=dev)
+    cur = torch.cuda.current_stream(dev)
+    main = _copy_stream(1)  # upload + decode (a stream of its own: see DESIGN.md §8)
+    main.wait_stream(cur)
+    cs = _copy_stream(0) if to_host else None
+    houts = [torch.empty(count, dtype=prec.torch_dtype, pin_memory=True) for _ in range(h.dims)] if to_host else None
+    if cs is not None:
+        cs.wait_stream(main)
+    done = 0
+    for k, (b0, b1) in enumerate(chunks):
+        end = n if b1 == h.block_count else h.table_end + int(tab[b1])
+        if end > done:
+            _par_memmove(stage.data_ptr() + done, host.ctypes.data + done, end - done)
+            with torch.cuda.stream(main):
+                t[done:end].copy_(stage[done:end], non_blocking=True)
+            done = end
+        _check(lib.gpzb_decompress_range_async(t.data_ptr(), n, ctypes.byref(h), ptrs, capacity, None,
+                                               ws.data_ptr(), ws.numel(), b0, b1, int(k == 0), main.cuda_stream))
+        if cs is not None:
+            e = torch.cuda.Event()
+            e.record(main)
+            cs.wait_event(e)
+            p0, p1 = b0 * bs, min(b1 * bs, count)
+            with torch.cuda.stream(cs):
+                for ho, o in zip(houts, outs):
+                    ho[p0:p1].copy_(o[p0:p1], non_blocking=True)
+    res = _lib.Result()
+    lib.gpzb_decompress_result(ws.data_ptr(), ws.numel(), ctypes.byref(h), main.cuda_stream, ctypes.byref(res))
+    if cs is not None:
+        cs.synchronize()
+    cur.wait_stream(main)  # (main is already idle: gpzb_decompress_result synchronised it)
+    _check(res.status, res)
+    if to_host:
+        return Dataset(axes=tuple(o.numpy() for o in houts), precision=prec)
+    return Dataset(axes=tuple(o[:count] for o in outs), precision=prec)
+
+
+def _streamed(data, to_host: bool):
+    """(_decode_streamed result) for host bytes-like containers, else None."""
+    if isinstance(data, torch.Tensor):
+        return None
+    host = _host_bytes(data)
+    if host.size < (32 << 20):
+        return None
+    h = parse_header(host[: _lib.GLOBAL_HEADER_SIZE].tobytes(), host.size)
+    plan = _streamed_plan(host, h)
+    if plan is None:
+        return None
+    return _decode_streamed(host, h, plan, to_host)
+
+
 def decompress_device(data, workers: int = 1, *, header=None, timing=None) -> Dataset:
     """Reconstruct on the GPU; the returned Dataset holds CUDA tensors.
 
@@ -425,6 +558,8 @@ def decompress_device(data, workers: int = 1, *, header=None, timing=None) -> Da
     del workers
     if header is not None and isinstance(data, torch.Tensor) and data.is_cuda:
         t, h = data, header
+    elif timing is None and (ds := _streamed(data, to_host=False)) is not None:
+        return ds
     else:
         t, h = _to_device_bytes(data)
     outs, res, _ = _decode(t, h, timing=timing)
@@ -439,8 +574,13 @@ def decompress(data, workers: int = 1) -> Dataset:
     Particles come back in sorted intra-block order unless the container
     preserves order; block boundaries always match the original.  The axes
     are numpy arrays over pinned host memory (PyTorch's caching host
-    allocator), filled by one device-to-host copy each.
+    allocator).  Containers of 32 MiB and more are decoded in chunks of
+    blocks so that the container's upload, the decode and the particles'
+    download overlap (_decode_streamed).
     """
+    ds = _streamed(data, to_host=True)
+    if ds is not None:
+        return ds
     ds = decompress_device(data, workers)
     outs = [torch.empty(a.numel(), dtype=a.dtype, pin_memory=True) for a in ds.axes]
     for o, a in zip(outs, ds.axes):
