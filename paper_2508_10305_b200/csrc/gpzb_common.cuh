@@ -183,6 +183,15 @@ __device__ __forceinline__ void red_or_shared(uint32_t* p, uint32_t v) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
+// The same, issued only where `p` holds (a predicated RED: no branch, no
+// convergence barrier around it).
+__device__ __forceinline__ void red_or_shared_if(bool p, uint32_t* a, uint32_t v) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.or.b32 [%0], %1;\n\t}" ::"r"(smem_u32(a)),
+      "r"(v), "r"((uint32_t)p)
+      : "memory");
+}
+
 // OR-reduction over the CTA of NV u32 values; result broadcast to all.
 template <int NV>
 __device__ __forceinline__ void block_or(uint32_t (&v)[NV], uint32_t* ws /* kWarps*NV */) {
@@ -212,7 +221,7 @@ __device__ __forceinline__ void block_or_z(uint32_t (&v)[NV], uint32_t* ws) {
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const uint32_t r = __reduce_or_sync(kFull, v[i]);
-    if (lane == 0 && r) red_or_shared(&ws[i], r);
+    red_or_shared_if(lane == 0 && r, &ws[i], r);
   }
   __syncthreads();
 #pragma unroll
@@ -335,15 +344,14 @@ __device__ __forceinline__ uint64_t quantize_coord(double x, const AxisGeo& g, d
 // ------------------------------------------------------ staging bit writer
 // OR `nbits` (<= 64) bits of v into a u32 word array at bit position pos.
 __device__ __forceinline__ void or_bits(uint32_t* st, uint64_t pos, uint64_t v) {
-  if (v == 0) return;
   const uint32_t sh = (uint32_t)(pos & 31);
   uint32_t* w = st + (pos >> 5);
   const uint64_t lo = v << sh;
   const uint32_t w0 = (uint32_t)lo, w1 = (uint32_t)(lo >> 32);
   const uint32_t w2 = sh ? (uint32_t)(v >> (64 - sh)) : 0u;
-  if (w0) red_or_shared(w, w0);
-  if (w1) red_or_shared(w + 1, w1);
-  if (w2) red_or_shared(w + 2, w2);
+  red_or_shared_if(w0 != 0, w, w0);
+  red_or_shared_if(w1 != 0, w + 1, w1);
+  red_or_shared_if(w2 != 0, w + 2, w2);
 }
 
 // Read `nbits` (<= 64) bits at bit position pos from a u32 word array.
