@@ -32,6 +32,9 @@ constexpr int kWarpDecWarps = GPZB_K4W_WARPS;  // warps per CTA
 // blocks with U <= GPZB_K4W_LUT_UMAX runs keep a midpoint table in the unused
 // tail of `uniq` (words 256..1023: 768 f32 / 384 f64 entries)
 constexpr int kWarpLutBase = 256, kWarpLutWords = kMaxBs - kWarpLutBase;
+// blocks without an offset stream (w_off = 0) and few runs keep each run's
+// reconstructed values there instead: [axis][run], kWarpRvStride runs per axis
+constexpr int kWarpRvStride = 256;
 struct WarpDecSmem {
   uint32_t win[kWinBytes / 4 + 8];
   __align__(16) uint32_t uniq[kMaxBs];     // run ids, or packed 10-bit table bases per axis + the table
@@ -42,7 +45,7 @@ constexpr size_t kWarpDecSmemBytes = sizeof(WarpDecSmem) * kWarpDecWarps;
 // The particle phase of K4w: 8 chunks of 128 positions, four consecutive
 // per lane (one 16-byte store per axis and chunk).  Q32: every bin index
 // < 2^31, so the 2^51 magic midpoint comes from one 32-bit word.
-template <int D, bool F64, bool Q32, bool LUT>
+template <int D, bool F64, bool Q32, bool LUT, bool RV = false>
 __device__ __forceinline__ uint32_t warp_particles(const DecParams& P, const WarpDecSmem& sm, uint64_t blk,
                                                    uint64_t idx_base, int lane, uint32_t wpre, uint32_t pbit,
                                                    uint32_t so, uint32_t wo, uint32_t sb, const double (&lo)[D],
@@ -60,8 +63,8 @@ __device__ __forceinline__ uint32_t warp_particles(const DecParams& P, const War
     const uint32_t word = sm.rstart[wsel];
     const uint32_t base = __shfl_sync(kFull, wpre, wsel);
     // the four offsets are adjacent in the stream: one or two 64-bit windows
-    uint32_t offs[4];
-    {
+    uint32_t offs[4] = {0, 0, 0, 0};
+    if constexpr (!RV) {
       const uint32_t pos = pbit + 8 * so + p0 * wo;
       const uint32_t* q = sm.win + (pos >> 5);
       const uint32_t sh = pos & 31;
@@ -80,6 +83,13 @@ __device__ __forceinline__ uint32_t warp_particles(const DecParams& P, const War
       const uint32_t b = (p0 + k) & 31;
       const uint32_t run = base + __popc(word & (0xffffffffu >> (31 - b))) - 1;
       const uint32_t off = offs[k];
+      if constexpr (RV) {
+        // no offset stream: every particle of a run has the run's values
+        const T* rvt = reinterpret_cast<const T*>(sm.uniq + kWarpLutBase);
+#pragma unroll
+        for (int a = 0; a < D; ++a) vals[a][k] = rvt[a * (F64 ? kWarpRvStride / 2 : kWarpRvStride) + run];
+        continue;
+      }
       if (sb < 32) offbad |= off >> sb;  // quantizer.py:264-265
       if constexpr (LUT) {
         // the run's table bases (bin seg_a << b_a of each axis) + this particle's offsets
@@ -184,7 +194,10 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
       const uint32_t used = cnt * w, nb = (used + 7) >> 3;
       if (w && cnt && (used & 7) && (pb[st + nb - 1] >> (used & 7))) fl |= 1u << lane;
     }
-    const bool wlut = U <= GPZB_K4W_LUT_UMAX && rec->lut_n != 0 && rec->lut_n <= (F64 ? kWarpLutWords / 2 : kWarpLutWords);
+    const bool rv = wo == 0 && U <= (F64 ? kWarpRvStride / 2 : kWarpRvStride) &&
+                    D * (F64 ? kWarpRvStride / 2 : kWarpRvStride) * (F64 ? 2 : 1) <= kWarpLutWords;
+    const bool wlut = !rv && U <= GPZB_K4W_LUT_UMAX && rec->lut_n != 0 &&
+                      rec->lut_n <= (F64 ? kWarpLutWords / 2 : kWarpLutWords);
     if (wlut) {  // every bin's midpoint, RN_T(lo + RN(RN(q + 0.5) w)) (quantizer.py:132-139)
       T* tab = reinterpret_cast<T*>(sm.uniq + kWarpLutBase);
       const uint32_t nt = rec->lut_n, l1 = rec->lut1, l2 = rec->lut2;
@@ -239,7 +252,27 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
         if (r > 0 && u <= prev) fl |= 1u << 3;  // pipeline.py:116-117
         if (cn < 1) fl |= 1u << 4;              // pipeline.py:118-119
         if (u >= rec->PN) fl |= 1u << 13;       // quantizer.py:262-263
-        if (wlut) {
+        if (rv) {
+          // the run's reconstruction per axis, as the midpoint table would hold it
+          T* rvt = reinterpret_cast<T*>(sm.uniq + kWarpLutBase);
+          uint32_t rest = (uint32_t)u;  // u < Π N <= 2^32 (else the block is reported below)
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            uint32_t sa;
+            if (a + 1 < D) {
+              const uint32_t qd = magic_div(rest, rec->mg_m[a], rec->mg_l[a]);
+              sa = rest - qd * rec->N[a];
+              rest = qd;
+            } else {
+              sa = rest;
+            }
+            const uint64_t qq = (uint64_t)sa << rec->b[a];
+            const double h = __longlong_as_double((long long)(0x4320000000000000ull + 2 * qq + 1));
+            rvt[a * (F64 ? kWarpRvStride / 2 : kWarpRvStride) + r] =
+                (T)__dadd_rn(rec->lo[a], __dmul_rn(__dsub_rn(h, 2251799813685248.0), rec->w[a]));
+          }
+          sm.uniq[r] = (uint32_t)u;
+        } else if (wlut) {
           uint32_t rest = (uint32_t)u, pk = 0;
 #pragma unroll
           for (int a = 0; a < D; ++a) {
@@ -302,7 +335,9 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
     const uint32_t sb = rec->sumb;
     const uint64_t idx_base = P.out_offsets ? P.out_offsets[blk] : blk * (uint64_t)P.bs;
     const uint32_t offbad =
-        wlut  ? warp_particles<D, F64, true, true>(P, sm, blk, idx_base, lane, wpre, pbit, so, wo, sb, lo, w, bsh,
+        rv    ? warp_particles<D, F64, true, false, true>(P, sm, blk, idx_base, lane, wpre, pbit, so, wo, sb, lo, w,
+                                                          bsh, shifts, Nn, mgm, mgl, omask)
+        : wlut  ? warp_particles<D, F64, true, true>(P, sm, blk, idx_base, lane, wpre, pbit, so, wo, sb, lo, w, bsh,
                                                    shifts, Nn, mgm, mgl, omask)
         : q32 ? warp_particles<D, F64, true, false>(P, sm, blk, idx_base, lane, wpre, pbit, so, wo, sb, lo, w, bsh,
                                                     shifts, Nn, mgm, mgl, omask)

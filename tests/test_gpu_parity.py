@@ -269,3 +269,28 @@ def test_batched_calls_match_single_calls():
     for c, r in zip(batch, recs):
         want = gz.decompress_device(c)
         assert all(torch.equal(x, y) for x, y in zip(r.axes, want.axes))
+
+
+@pytest.mark.parametrize("prec,dims", [(O.F32, 3), (O.F64, 3), (O.F64, 2), (O.F32, 1)])
+def test_offset_free_warp_blocks(prec, dims):
+    """Full blocks with no offset stream (every log2 m = 0) and few runs take
+    K4w's run-values body (each run's reconstruction computed once); the
+    result must be the oracle's, bit for bit, in every precision."""
+    rng = np.random.default_rng(40 + dims)
+    dt = np.float64 if prec == O.F64 else np.float32
+    centers = rng.uniform(0, 1, size=(8, dims))  # one tight cluster per block: Q_a <= t, so log2 m = 0
+    axes = [(np.repeat(centers[:, a], 1024) + rng.normal(0, 0.001, 8192)).astype(dt) for a in range(dims)]
+    blob = O.compress(axes, O.Config(1e-3))
+    h, table, _ = O.read_container(blob)
+    assert gz.compress(gz.Dataset.from_axes(axes), gz.CompressConfig(1e-3)) == blob
+    rec = gz.decompress(blob)
+    for x, y in zip(rec.axes, O.decompress(blob)):
+        assert np.array_equal(x, y)
+    # the case is what it claims: no offsets, few runs
+    base = 46 + 8 * (h.blocks + 1)
+    for i in range(h.blocks):
+        blk = blob[base + int(table[i]): base + int(table[i + 1])]
+        S = 8 if prec == O.F64 else 4
+        wpos = 8 + dims * (2 * S + 5)
+        assert blk[wpos + 2] == 0  # w_off
+        assert int.from_bytes(blk[4:8], "little") <= (128 if prec == O.F64 else 256)
