@@ -27,6 +27,9 @@ namespace gpzb {
 #ifndef GPZB_K2P_MINB
 #define GPZB_K2P_MINB 5
 #endif
+#ifndef GPZB_K2P_L2PF
+#define GPZB_K2P_L2PF 1  // blocks ahead (in this warp's sequence) to bulk-prefetch into L2; 0 = off
+#endif
 constexpr int kWarpEncWarps = GPZB_K2P_WARPS;
 // payload <= 74 + 1024 * (14 + 11) / 8 + 2 = 3,276 bytes (widths <= bitlen(16383), bitlen(1024))
 constexpr int kWarpStageWords = 832;
@@ -55,6 +58,18 @@ __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_wa
     const BlkRec* rec = P.rec + blk;
     if (rec->kind != KIND_WARP) continue;  // warp-uniform
     const uint64_t first = blk * (uint64_t)P.bs;
+#if GPZB_K2P_L2PF
+    // the next block's coordinates into L2 (one bulk prefetch per axis): its
+    // loads then wait on L2, not HBM, while this block ranks and packs
+    if (lane < D && blk + GPZB_K2P_L2PF * stride < P.nblocks && P.vec) {
+      const uint64_t nf = (blk + GPZB_K2P_L2PF * stride) * (uint64_t)P.bs;
+      const uint32_t nbytes = (uint32_t)((min((uint64_t)P.bs, P.count - nf) * S) & ~15ull);
+      if (nbytes)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const T*>(P.axes[lane]) + nf),
+                     "r"(nbytes)
+                     : "memory");
+    }
+#endif
     const uint32_t PN = rec->PN;
     const uint32_t nw = (PN + 31) >> 5;
     // ---- zero the bitmap and the run counters
