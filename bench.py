@@ -227,17 +227,25 @@ def main():
         b = torch.cuda.Event(enable_timing=True)
         c = torch.cuda.Event(enable_timing=True)
         a.record()
-        conts = gz.compress_batch_device(datasets, cfg, timing=timing)
+        if world > 1:  # this rank's shard of each field; scalar exchanges batched over the fields
+            conts = sharded.compress_batch_device(datasets, cfg, timing=timing)
+        else:
+            conts = gz.compress_batch_device(datasets, cfg, timing=timing)
         b.record()
-        recs = None if args.compress_only else gz.decompress_batch_device(conts, timing=timing)
+        if args.compress_only:
+            recs = None
+        elif world > 1:
+            recs = sharded.decompress_batch_device(conts, timing=timing)
+        else:
+            recs = gz.decompress_batch_device(conts, timing=timing)
         c.record()
         torch.cuda.synchronize()
-        sizes = [x.numel() for x in conts]
+        sizes = [x.local_bytes if world > 1 else x.numel() for x in conts]
         del conts, recs
         return a.elapsed_time(b) / 1e3, b.elapsed_time(c) / 1e3, sizes
 
     def one_step(timing=None):
-        if world == 1 and not args.per_call:
+        if not args.per_call:
             return one_step_batch(timing)
         sizes, recs = [], []
         tc = td = 0.0

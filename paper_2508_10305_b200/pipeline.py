@@ -128,8 +128,9 @@ def _ev():
     return e
 
 
-def _compress_begin(ds, cfg: CompressConfig, slot: int, timing) -> _Job:
-    """Allocate and enqueue the workspace reset, K1 and K1.5 (no host sync)."""
+def _compress_begin(ds, cfg: CompressConfig, slot: int, timing, plan: bool = True) -> _Job:
+    """Allocate and enqueue the workspace reset, K1 and K1.5 (no host sync).
+    plan=False stops after K1 (sharded runs reduce the range words first)."""
     j = _Job()
     ds = _as_dataset(ds)
     j.axes = _device_axes(ds)
@@ -155,9 +156,16 @@ def _compress_begin(ds, cfg: CompressConfig, slot: int, timing) -> _Job:
     _check(lib.gpzb_range_async(j.ptrs, j.dims, j.prec, j.count, j.bs, j.ws.data_ptr(), j.ws.numel(), j.stream))
     if timing is not None:
         timing.setdefault("range", []).append((e0, _ev()))
-    _check(lib.gpzb_encode_plan_async(j.ptrs, j.dims, j.prec, j.count, j.eb, j.mode, j.bs, j.t, j.pres,
-                                      j.ws.data_ptr(), j.ws.numel(), j.stream))
+    if plan:
+        _compress_plan(j)
     return j
+
+
+def _compress_plan(j: _Job) -> None:
+    """Enqueue K1.5 (bound resolution from the range words + block routing)."""
+    if j.count:
+        _check(lib.gpzb_encode_plan_async(j.ptrs, j.dims, j.prec, j.count, j.eb, j.mode, j.bs, j.t, j.pres,
+                                          j.ws.data_ptr(), j.ws.numel(), j.stream))
 
 
 def _compress_encode(j: _Job) -> None:
@@ -176,13 +184,17 @@ def _compress_encode(j: _Job) -> None:
         j.timing.setdefault("encode", []).append((e0, _ev()))
 
 
+def _compress_status(j: _Job) -> int:
+    """Read the result record (one sync of the job's stream); no raising."""
+    if j.count == 0:
+        return lib.gpzb_compress(j.ptrs, j.dims, j.prec, j.count, j.eb, j.mode, j.bs, j.t, j.pres, j.ws.data_ptr(),
+                                 j.ws.numel(), j.out.data_ptr(), j.bound, j.stream, ctypes.byref(j.res))
+    return lib.gpzb_compress_result(j.ws.data_ptr(), j.ws.numel(), j.count, j.bs, j.stream, ctypes.byref(j.res))
+
+
 def _compress_finish(j: _Job) -> torch.Tensor:
     """Read the result record (one sync) and map errors."""
-    if j.count == 0:
-        st = lib.gpzb_compress(j.ptrs, j.dims, j.prec, j.count, j.eb, j.mode, j.bs, j.t, j.pres, j.ws.data_ptr(),
-                               j.ws.numel(), j.out.data_ptr(), j.bound, j.stream, ctypes.byref(j.res))
-    else:
-        st = lib.gpzb_compress_result(j.ws.data_ptr(), j.ws.numel(), j.count, j.bs, j.stream, ctypes.byref(j.res))
+    st = _compress_status(j)
     _check(st, j.res)
     compress_device.last_result = j.res
     _LAST.update(ws=j.ws, count=j.count, bs=j.bs, dims=j.dims, prec=j.prec)

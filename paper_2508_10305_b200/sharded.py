@@ -180,6 +180,94 @@ def compress_device(ds: Dataset, cfg: CompressConfig, *, timing=None, hooks=None
                             global_payload=sum(totals))
 
 
+def compress_batch_device(datasets, cfg: CompressConfig, *, timing=None) -> list:
+    """compress_device over several datasets (the fields of one snapshot) with
+    one CUDA stream + workspace each, as pipeline.compress_batch_device, and
+    ONE collective per exchange for all of them: the shard counts, the range
+    words (REL), and the (first error, payload total) records.  Returns one
+    ShardedContainer per dataset, each identical to compress_device's."""
+    from .pipeline import _check, _compress_begin, _compress_encode, _compress_plan, _compress_status, _side_stream
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    bs = cfg.block_size
+    k = len(datasets)
+    dev = _comm_device()
+    t = torch.tensor([d.count for d in datasets], dtype=torch.int64, device=dev)
+    allc = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(allc, t)
+    counts = torch.stack(allc).cpu().tolist()  # [rank][dataset]
+    for r in range(world - 1):
+        for i in range(k):
+            if counts[r][i] % bs:
+                raise ValueError(f"rank {r} holds {counts[r][i]} particles, not a multiple of block_size {bs}")
+    cur = torch.cuda.current_stream()
+    start = torch.cuda.Event()
+    start.record(cur)
+    jobs = []
+    for i, ds in enumerate(datasets):
+        s = _side_stream(i)
+        s.wait_event(start)
+        with torch.cuda.stream(s):
+            jobs.append(_compress_begin(ds, cfg, i, timing, plan=False))
+    if cfg.eb_mode is EbMode.RANGE_RELATIVE:
+        live = [j for j in jobs if j.count]
+        for i in range(k):
+            cur.wait_stream(_side_stream(i))
+        if live:
+            words = torch.stack([j.ws[40:56].view(torch.int64) for j in live])  # DevResult.range_w of each
+            _allreduce_max_words(words)
+            for j, w in zip(live, words):
+                j.ws[40:56].view(torch.int64).copy_(w)
+        for i in range(k):
+            _side_stream(i).wait_stream(cur)
+    for i, j in enumerate(jobs):
+        with torch.cuda.stream(_side_stream(i)):
+            _compress_plan(j)
+    for i, j in enumerate(jobs):
+        with torch.cuda.stream(_side_stream(i)):
+            _compress_encode(j)
+    inf = 1 << 62
+    rows, locals_ = [], []
+    for i, j in enumerate(jobs):
+        with torch.cuda.stream(_side_stream(i)):
+            st = _compress_status(j)
+        cur.wait_stream(_side_stream(i))
+        first_block = sum((c[i] + bs - 1) // bs for c in counts[:rank])
+        key = inf if st == 0 else (-1 if j.res.block < 0 else first_block + j.res.block)
+        local = j.out[: j.res.out_len] if st == 0 else None
+        if local is not None:
+            local.record_stream(cur)
+        payload = (int(local.numel()) - 46 - 8 * (j.nb + 1)) if local is not None else 0
+        rows.append([key, st, j.res.reason, j.res.axis, payload])
+        locals_.append(local)
+    info = torch.tensor(rows, dtype=torch.int64, device=dev)
+    alli = [torch.zeros_like(info) for _ in range(world)]
+    dist.all_gather(alli, info)
+    alli = torch.stack(alli).cpu().tolist()  # [rank][dataset][5]
+    out = []
+    for i, (ds, j) in enumerate(zip(datasets, jobs)):
+        win = min((alli[r][i] for r in range(world)), key=lambda v: v[0])
+        if win[0] != inf:
+            key, wst, wreason, waxis, _ = win
+            _check(wst, _lib.Result(status=wst, reason=wreason, block=key, axis=waxis))
+        totals = [alli[r][i][4] for r in range(world)]
+        g_count = sum(c[i] for c in counts)
+        g_blocks = sum((c[i] + bs - 1) // bs for c in counts)
+        header = _header(ds.dims, ds.precision.value, cfg, float(j.res.eb_abs), g_count, g_blocks)
+        out.append(ShardedContainer(local=locals_[i], rank=rank, world=world, base=sum(totals[:rank]),
+                                    first_block=sum((c[i] + bs - 1) // bs for c in counts[:rank]),
+                                    global_count=g_count, global_blocks=g_blocks, local_blocks=j.nb,
+                                    header=header, global_payload=sum(totals)))
+    return out
+
+
+def decompress_batch_device(scs: list, *, timing=None) -> list:
+    """Each rank decodes its own blocks of every container (no exchange)."""
+    from .pipeline import decompress_batch_device as dbd
+
+    return dbd([sc.local for sc in scs], timing=timing)
+
+
 def _comm_device():
     if dist.get_backend() == "nccl":
         return torch.device("cuda", torch.cuda.current_device())

@@ -191,3 +191,70 @@ def test_sharded_cuda_hooks_two_ranks_one_gpu(tmp_path):
     for p in procs:
         p.join(timeout=60)
     assert out == [(0, True, True, True), (1, True, True, True)], out
+
+
+def _run_cuda_batch(rank, world, port, q):
+    """sharded.compress_batch_device over two fields (one stream each, one
+    collective per exchange): every container equals the single-process one."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import paper_2508_10305_b200 as gz
+        from paper_2508_10305_b200 import sharded
+
+        rng = np.random.default_rng(5)
+        pos = O.gen_clusters(300_000, dims=3, seed=22)
+        vel = [(rng.normal(0, 0.3, 300_000) + rng.normal(0, 0.05, 300_000)).astype(np.float32) for _ in range(3)]
+        cut = 150 * 1024
+        sl = slice(0, cut) if rank == 0 else slice(cut, None)
+        shards = [gz.Dataset.from_axes([torch.from_numpy(a[sl].copy()).cuda() for a in f]) for f in (pos, vel)]
+        ok = []
+        for mode in (gz.EbMode.RANGE_RELATIVE, gz.EbMode.ABSOLUTE):
+            cfg = gz.CompressConfig(error_bound=1e-3, eb_mode=mode)
+            scs = sharded.compress_batch_device(shards, cfg)
+            blobs = [sharded.to_global_bytes(sc) for sc in scs]
+            recs = sharded.decompress_batch_device(scs)
+            for f, blob, rec in zip((pos, vel), blobs, recs):
+                want = gz.compress(gz.Dataset.from_axes(f), cfg)
+                full_rec = gz.decompress(want)
+                ok.append(all(np.array_equal(r.cpu().numpy(), w[sl]) for r, w in zip(rec.axes, full_rec.axes)))
+                if rank == 0:
+                    ok.append(blob == want)
+        # an overflowing block on rank 1 (second field): every rank raises the
+        # single-process error, global block index included
+        bad = [a.copy() for a in vel]
+        bad[1][cut + 5000] = 3e38
+        cfg = gz.CompressConfig(error_bound=1e-6, eb_mode=gz.EbMode.ABSOLUTE)
+        shards[1] = gz.Dataset.from_axes([torch.from_numpy(a[sl].copy()).cuda() for a in bad])
+        try:
+            gz.compress(gz.Dataset.from_axes(bad), cfg)
+            want_err = None
+        except gz.GpzError as exc:
+            want_err = (type(exc).__name__, str(exc))
+        try:
+            sharded.compress_batch_device(shards, cfg)
+            got_err = None
+        except gz.GpzError as exc:
+            got_err = (type(exc).__name__, str(exc))
+        ok.append(want_err is not None and got_err == want_err)
+        q.put((rank, all(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_batch_two_ranks_one_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_run_cuda_batch, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert out == [(0, True), (1, True)], out
