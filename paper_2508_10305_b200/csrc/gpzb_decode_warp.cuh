@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
     const uint32_t U = rec->U;
     const uint32_t wd = rec->wd, wc = rec->wc, wo = rec->wo;
     const uint32_t sd = rec->sd, sc = rec->sc, so = rec->so;
+    const uint32_t PN = rec->PN;  // held in a register: the run loop's shared-memory REDs would force reloads
     const uint8_t* pay = P.c + P.table_end + rec->e0;
     const uint32_t al = (uint32_t)((uintptr_t)pay & 15);
     const uint32_t plen = so + ((kMaxBs * wo + 7) >> 3);
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
         const uint64_t u = prev + dl;
         if (r > 0 && u <= prev) fl |= 1u << 3;  // pipeline.py:116-117
         if (cn < 1) fl |= 1u << 4;              // pipeline.py:118-119
-        if (u >= rec->PN) fl |= 1u << 13;       // quantizer.py:262-263
+        if (u >= PN) fl |= 1u << 13;            // quantizer.py:262-263
         if (rv) {
           // the run's reconstruction per axis, as the midpoint table would hold it
           T* rvt = reinterpret_cast<T*>(sm.uniq + kWarpLutBase);
