@@ -216,12 +216,33 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
     uint32_t csum = 0;
     // narrow streams: keep each run's (delta, count) from this pass in uniq[r]
     const bool keep = wd <= 16 && wc <= 16;
-    for (uint32_t r = r0; r < r1; ++r) {
-      const uint32_t dl = get_bits32(sm.win, pbit + 8 * sd + r * wd, wd);
-      const uint32_t cn = get_bits32(sm.win, pbit + 8 * sc + r * wc, wc);
-      dsum += dl;
-      csum += cn;
-      if (keep) sm.uniq[r] = dl | (cn << 16);
+    if (keep) {
+      // two runs per 32-bit funnel window of each stream (widths <= 16)
+      const uint32_t md = (1u << wd) - 1u, mc = (1u << wc) - 1u;
+      uint32_t pd = pbit + 8 * sd + r0 * wd, pc = pbit + 8 * sc + r0 * wc;
+      uint32_t r = r0;
+      for (; r + 1 < r1; r += 2, pd += 2 * wd, pc += 2 * wc) {
+        const uint32_t vd = __funnelshift_r(sm.win[pd >> 5], sm.win[(pd >> 5) + 1], pd & 31);
+        const uint32_t vc = __funnelshift_r(sm.win[pc >> 5], sm.win[(pc >> 5) + 1], pc & 31);
+        const uint32_t d0 = vd & md, d1 = (vd >> wd) & md, c0 = vc & mc, c1 = (vc >> wc) & mc;
+        dsum += d0 + d1;
+        csum += c0 + c1;
+        sm.uniq[r] = d0 | (c0 << 16);
+        sm.uniq[r + 1] = d1 | (c1 << 16);
+      }
+      if (r < r1) {
+        const uint32_t dl = get_bits32(sm.win, pd, wd), cn = get_bits32(sm.win, pc, wc);
+        dsum += dl;
+        csum += cn;
+        sm.uniq[r] = dl | (cn << 16);
+      }
+    } else {
+      for (uint32_t r = r0; r < r1; ++r) {
+        const uint32_t dl = get_bits32(sm.win, pbit + 8 * sd + r * wd, wd);
+        const uint32_t cn = get_bits32(sm.win, pbit + 8 * sc + r * wc, wc);
+        dsum += dl;
+        csum += cn;
+      }
     }
     // packed warp scan (Σ deltas < 2^42 in the low 43 bits; run lengths,
     // clamped per lane at 1025, above them: a valid block sums to 1024)
@@ -237,7 +258,13 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
     const unsigned long long ctot = __shfl_sync(kFull, incl, 31) >> kDBits;
     {
       const unsigned long long ex = incl - mine;
-      uint64_t prev = ex & kDMask;
+      // ids are prefix sums of non-negative deltas, so (pipeline.py:116-119,
+      // quantizer.py:262-263): a later id not above its predecessor <=> a zero
+      // delta; an id >= Π N anywhere <=> this lane's last id >= Π N (checked in
+      // 64 bits once; inside the loop 32-bit ids are exact whenever it passes)
+      const uint64_t prev0 = ex & kDMask;
+      if (r1 > r0 && prev0 + dsum >= PN) fl |= 1u << 13;
+      uint32_t uu = (uint32_t)prev0, mn_dl = 0xffffffffu, mn_cn = 0xffffffffu;
       uint32_t cex = (uint32_t)(ex >> kDBits);
       for (uint32_t r = r0; r < r1; ++r) {
         uint32_t dl, cn;
@@ -249,14 +276,13 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
           dl = get_bits32(sm.win, pbit + 8 * sd + r * wd, wd);
           cn = get_bits32(sm.win, pbit + 8 * sc + r * wc, wc);
         }
-        const uint64_t u = prev + dl;
-        if (r > 0 && u <= prev) fl |= 1u << 3;  // pipeline.py:116-117
-        if (cn < 1) fl |= 1u << 4;              // pipeline.py:118-119
-        if (u >= PN) fl |= 1u << 13;            // quantizer.py:262-263
+        uu += dl;
+        mn_dl = min(mn_dl, r ? dl : 0xffffffffu);
+        mn_cn = min(mn_cn, cn);
         if (rv) {
           // the run's reconstruction per axis, as the midpoint table would hold it
           T* rvt = reinterpret_cast<T*>(sm.uniq + kWarpLutBase);
-          uint32_t rest = (uint32_t)u;  // u < Π N <= 2^32 (else the block is reported below)
+          uint32_t rest = uu;  // u < Π N <= 2^32 (else the block is reported below)
 #pragma unroll
           for (int a = 0; a < D; ++a) {
             uint32_t sa;
@@ -272,9 +298,9 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
             rvt[a * (F64 ? kWarpRvStride / 2 : kWarpRvStride) + r] =
                 (T)__dadd_rn(rec->lo[a], __dmul_rn(__dsub_rn(h, 2251799813685248.0), rec->w[a]));
           }
-          sm.uniq[r] = (uint32_t)u;
+          sm.uniq[r] = uu;
         } else if (wlut) {
-          uint32_t rest = (uint32_t)u, pk = 0;
+          uint32_t rest = uu, pk = 0;
 #pragma unroll
           for (int a = 0; a < D; ++a) {
             uint32_t sa;
@@ -290,12 +316,13 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
           }
           sm.uniq[r] = pk;
         } else {
-          sm.uniq[r] = (uint32_t)u;
+          sm.uniq[r] = uu;
         }
-        if (cex < (uint32_t)kMaxBs) red_or_shared(&sm.rstart[cex >> 5], 1u << (cex & 31));
+        red_or_shared_if(cex < (uint32_t)kMaxBs, &sm.rstart[cex >> 5], 1u << (cex & 31));
         cex += cn;
-        prev = u;
       }
+      if (mn_dl == 0) fl |= 1u << 3;  // pipeline.py:116-117
+      if (mn_cn == 0) fl |= 1u << 4;  // pipeline.py:118-119
     }
     if (ctot != (unsigned long long)kMaxBs) fl |= 1u << 5;  // pipeline.py:120-123
     fl = __reduce_or_sync(kFull, fl);
