@@ -56,12 +56,21 @@ __device__ __forceinline__ uint32_t warp_particles(const DecParams& P, const War
   using T = typename std::conditional<F64, double, float>::type;
   uint32_t offbad = 0;
   const uint32_t omask4 = wo >= 32 ? 0xffffffffu : (1u << wo) - 1u;
+  // a particle's run = run starts at or before it - 1; its bit in the map
+  // word is (4 lane + k) mod 32 in every chunk
+  uint32_t below[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) below[k] = 0xffffffffu >> (31 - ((4 * lane + k) & 31));
+  // whole-block 16-byte stores when every axis is aligned and the block fits
+  bool vec_ok = idx_base + kMaxBs <= P.out_cap;
+#pragma unroll
+  for (int a = 0; a < D; ++a) vec_ok = vec_ok && ((reinterpret_cast<uintptr_t>(reinterpret_cast<T*>(P.out[a]) + idx_base) & 15) == 0);
 #pragma unroll 1
   for (int c = 0; c < kMaxBs / 128; ++c) {
     const uint32_t p0 = c * 128 + 4 * lane;
     const uint32_t wsel = p0 >> 5;  // the four share one map word
     const uint32_t word = sm.rstart[wsel];
-    const uint32_t base = __shfl_sync(kFull, wpre, wsel);
+    const uint32_t base = __shfl_sync(kFull, wpre, wsel) - 1u;
     // the four offsets are adjacent in the stream: one or two 64-bit windows
     uint32_t offs[4] = {0, 0, 0, 0};
     if constexpr (!RV) {
@@ -76,12 +85,12 @@ __device__ __forceinline__ uint32_t warp_particles(const DecParams& P, const War
 #pragma unroll
         for (int k = 0; k < 4; ++k) offs[k] = get_bits32(sm.win, pos + k * wo, wo);
       }
+      if (sb < 32) offbad |= (offs[0] | offs[1] | offs[2] | offs[3]) >> sb;  // quantizer.py:264-265
     }
     T vals[D][4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint32_t b = (p0 + k) & 31;
-      const uint32_t run = base + __popc(word & (0xffffffffu >> (31 - b))) - 1;
+      const uint32_t run = base + __popc(word & below[k]);
       const uint32_t off = offs[k];
       if constexpr (RV) {
         // no offset stream: every particle of a run has the run's values
@@ -90,7 +99,6 @@ __device__ __forceinline__ uint32_t warp_particles(const DecParams& P, const War
         for (int a = 0; a < D; ++a) vals[a][k] = rvt[a * (F64 ? kWarpRvStride / 2 : kWarpRvStride) + run];
         continue;
       }
-      if (sb < 32) offbad |= off >> sb;  // quantizer.py:264-265
       if constexpr (LUT) {
         // the run's table bases (bin seg_a << b_a of each axis) + this particle's offsets
         const uint32_t pk = sm.uniq[run];
@@ -128,7 +136,7 @@ __device__ __forceinline__ uint32_t warp_particles(const DecParams& P, const War
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       T* out = reinterpret_cast<T*>(P.out[a]);
-      if (idx0 + 4 <= P.out_cap && ((reinterpret_cast<uintptr_t>(out + idx0) & 15) == 0)) {
+      if (vec_ok) {
         if constexpr (sizeof(T) == 4) {
           __stcs(reinterpret_cast<float4*>(out + idx0), make_float4(vals[a][0], vals[a][1], vals[a][2], vals[a][3]));
         } else {
