@@ -354,6 +354,15 @@ __device__ __forceinline__ void or_bits(uint32_t* st, uint64_t pos, uint64_t v) 
   red_or_shared_if(w2 != 0, w + 2, w2);
 }
 
+// The same for a value of at most 32 bits: two predicated REDs, 32-bit shifts.
+__device__ __forceinline__ void or_bits32(uint32_t* st, uint32_t pos, uint32_t v) {
+  const uint32_t sh = pos & 31;
+  uint32_t* w = st + (pos >> 5);
+  const uint32_t w0 = v << sh, w1 = sh ? v >> (32 - sh) : 0u;
+  red_or_shared_if(w0 != 0, w, w0);
+  red_or_shared_if(w1 != 0, w + 1, w1);
+}
+
 // Read `nbits` (<= 64) bits at bit position pos from a u32 word array.
 __device__ __forceinline__ uint64_t get_bits(const uint32_t* st, uint64_t pos, uint32_t nbits) {
   if (nbits == 0) return 0;

@@ -386,32 +386,47 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
       if (act) or_bits(st, 8ull * bpos, val);
     }
     const uint64_t bd = 8ull * H, bc = bd + 8ull * Ld, bo = bc + 8ull * Lc;
-    // deltas + run lengths, 4 consecutive runs per chunk
+    // deltas + run lengths, 4 consecutive runs per chunk (32-bit windows
+    // when four values fit in 32 bits, else 64-bit ones)
+    const bool d32 = 4 * w_del <= 32, c32 = 4 * w_cnt <= 32;
     for (uint32_t r0 = 4 * t; r0 < U; r0 += 4 * nt) {
-      uint64_t dv = 0, cv = 0;
+      uint32_t d[4], cn[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint32_t r = r0 + j;
-        if (r < U) {
-          const uint32_t d = (uint32_t)sm.uniqp[r + 1] - (uint32_t)sm.uniqp[r];
-          dv |= (uint64_t)d << (j * w_del);
-          cv |= (uint64_t)sm.cnt[r] << (j * w_cnt);
-        }
+        d[j] = r < U ? (uint32_t)sm.uniqp[r + 1] - (uint32_t)sm.uniqp[r] : 0u;
+        cn[j] = r < U ? sm.cnt[r] : 0u;
       }
-      if (w_del) or_bits(st, bd + (uint64_t)r0 * w_del, dv);
-      if (w_cnt) or_bits(st, bc + (uint64_t)r0 * w_cnt, cv);
+      if (d32) {
+        if (w_del) or_bits32(st, (uint32_t)bd + r0 * w_del, d[0] | d[1] << w_del | d[2] << (2 * w_del) | d[3] << (3 * w_del));
+      } else {
+        uint64_t dv = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dv |= (uint64_t)d[j] << (j * w_del);
+        or_bits(st, bd + (uint64_t)r0 * w_del, dv);
+      }
+      if (c32) {
+        if (w_cnt) or_bits32(st, (uint32_t)bc + r0 * w_cnt, cn[0] | cn[1] << w_cnt | cn[2] << (2 * w_cnt) | cn[3] << (3 * w_cnt));
+      } else {
+        uint64_t cv = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cv |= (uint64_t)cn[j] << (j * w_cnt);
+        or_bits(st, bc + (uint64_t)r0 * w_cnt, cv);
+      }
     }
-    // offsets in sorted order, 4 per chunk (two 2-value halves when w_off > 16)
+    // offsets in sorted order, 4 per chunk: one 32-bit window when they fit,
+    // else two 2-value 64-bit halves
     if (w_off) {
       for (uint32_t p = 4 * t; p < (uint32_t)n; p += 4 * nt) {
-        uint64_t v0 = 0, v1 = 0;
+        uint32_t o[4];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          if (p + j < (uint32_t)n) v0 |= (uint64_t)sm.soff[p + j] << (j * w_off);
-          if (p + 2 + j < (uint32_t)n) v1 |= (uint64_t)sm.soff[p + 2 + j] << (j * w_off);
+        for (int j = 0; j < 4; ++j) o[j] = p + j < (uint32_t)n ? sm.soff[p + j] : 0u;
+        if (4 * w_off <= 32) {
+          or_bits32(st, (uint32_t)bo + p * w_off, o[0] | o[1] << w_off | o[2] << (2 * w_off) | o[3] << (3 * w_off));
+        } else {
+          or_bits(st, bo + (uint64_t)p * w_off, (uint64_t)o[0] | (uint64_t)o[1] << w_off);
+          or_bits(st, bo + (uint64_t)(p + 2) * w_off, (uint64_t)o[2] | (uint64_t)o[3] << w_off);
         }
-        or_bits(st, bo + (uint64_t)p * w_off, v0);
-        or_bits(st, bo + (uint64_t)(p + 2) * w_off, v1);
       }
     }
   }
