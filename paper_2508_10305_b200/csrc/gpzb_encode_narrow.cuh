@@ -174,16 +174,21 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
   __syncthreads();
 
   // ---- 3. stream widths (width_for == bit length of the OR) and payload size
-  uint32_t cloc[kItems], csum = 0, c_or = 0, d_or = 0;
+  // this thread's runs p0..p0+3 are also the ones it packs in step 5: keep
+  // each run's delta | count << 16 (delta < 2^16, count <= 1024) in registers
+  uint32_t cloc[kItems], dc[kItems], csum = 0, c_or = 0, d_or = 0;
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const uint32_t r = p0 + j;
     cloc[j] = 0;
+    dc[j] = 0;
     if (r < U) {
       cloc[j] = sm.cnt[r];
+      const uint32_t d = (uint32_t)sm.uniqp[r + 1] - (uint32_t)sm.uniqp[r];
       c_or |= cloc[j];
-      d_or |= (uint32_t)sm.uniqp[r + 1] - (uint32_t)sm.uniqp[r];
+      d_or |= d;
       csum += cloc[j];
+      dc[j] = d | (cloc[j] << 16);
     }
   }
   uint32_t red[3] = {off_or, c_or, d_or};
@@ -389,13 +394,14 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
     // deltas + run lengths, 4 consecutive runs per chunk (32-bit windows
     // when four values fit in 32 bits, else 64-bit ones)
     const bool d32 = 4 * w_del <= 32, c32 = 4 * w_cnt <= 32;
-    for (uint32_t r0 = 4 * t; r0 < U; r0 += 4 * nt) {
+    static_assert(kItems == 4 && kThreads * kItems >= kMaxBs, "one chunk of four runs per thread");
+    if (p0 < (int)U) {
+      const uint32_t r0 = p0;
       uint32_t d[4], cn[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const uint32_t r = r0 + j;
-        d[j] = r < U ? (uint32_t)sm.uniqp[r + 1] - (uint32_t)sm.uniqp[r] : 0u;
-        cn[j] = r < U ? sm.cnt[r] : 0u;
+        d[j] = dc[j] & 0xffffu;
+        cn[j] = dc[j] >> 16;
       }
       if (d32) {
         if (w_del) or_bits32(st, (uint32_t)bd + r0 * w_del, d[0] | d[1] << w_del | d[2] << (2 * w_del) | d[3] << (3 * w_del));
