@@ -61,6 +61,14 @@ __device__ __forceinline__ uint32_t warp_particles(const DecParams& P, const War
   uint32_t below[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) below[k] = 0xffffffffu >> (31 - ((4 * lane + k) & 31));
+  // Q32: 2q + 1 = (s << (b + 1) | 1) | (o << 1), built as s * 2^(b+1) + 1 and a
+  // funnel shift of the particle's offsets already doubled (q < 2^31: no overflow)
+  uint32_t mul1[D], om2[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    mul1[a] = bsh[a] >= 31 ? 0u : 1u << (bsh[a] + 1);
+    om2[a] = omask[a] << 1;
+  }
   // whole-block 16-byte stores when every axis is aligned and the block fits
   bool vec_ok = idx_base + kMaxBs <= P.out_cap;
 #pragma unroll
@@ -119,11 +127,12 @@ __device__ __forceinline__ uint32_t warp_particles(const DecParams& P, const War
         } else {
           sa = rest;
         }
-        const uint32_t oa = (off >> shifts[a]) & omask[a];
         double h;
         if constexpr (Q32) {
-          h = __hiloint2double(0x43200000, (int)(2u * ((sa << bsh[a]) | oa) + 1u));
+          const uint32_t o2 = __funnelshift_r(off << 1, off >> 31, shifts[a]) & om2[a];
+          h = __hiloint2double(0x43200000, (int)((sa * mul1[a] + 1u) | o2));
         } else {
+          const uint32_t oa = (off >> shifts[a]) & omask[a];
           const uint64_t qq = ((uint64_t)sa << bsh[a]) | oa;
           h = __longlong_as_double((long long)(0x4320000000000000ull + 2 * qq + 1));
         }
