@@ -176,19 +176,18 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
   // ---- 3. stream widths (width_for == bit length of the OR) and payload size
   // this thread's runs p0..p0+3 are also the ones it packs in step 5: keep
   // each run's delta | count << 16 (delta < 2^16, count <= 1024) in registers
-  uint32_t cloc[kItems], dc[kItems], csum = 0, c_or = 0, d_or = 0;
+  uint32_t dc[kItems], csum = 0, c_or = 0, d_or = 0;
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const uint32_t r = p0 + j;
-    cloc[j] = 0;
     dc[j] = 0;
     if (r < U) {
-      cloc[j] = sm.cnt[r];
+      const uint32_t c = sm.cnt[r];
       const uint32_t d = (uint32_t)sm.uniqp[r + 1] - (uint32_t)sm.uniqp[r];
-      c_or |= cloc[j];
+      c_or |= c;
       d_or |= d;
-      csum += cloc[j];
-      dc[j] = d | (cloc[j] << 16);
+      csum += c;
+      dc[j] = d | (c << 16);
     }
   }
   uint32_t red[3] = {off_or, c_or, d_or};
@@ -217,7 +216,7 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
 #pragma unroll
       for (int j = 0; j < kItems; ++j) {
         if (p0 + j < (int)U) sm.u.g.segstart[p0 + j] = (uint16_t)ex;
-        ex += cloc[j];
+        ex += dc[j] >> 16;
       }
       uint32_t code[kItems];
 #pragma unroll
@@ -297,7 +296,7 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
 #pragma unroll
       for (int j = 0; j < kItems; ++j) {
         if (p0 + j < (int)U) sm.u.c.segstart[p0 + j] = (uint16_t)ex;
-        ex += cloc[j];
+        ex += dc[j] >> 16;
       }
       __syncthreads();
       uint32_t g0[kItems];
