@@ -131,12 +131,12 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
       stride *= rec->N[a];
       shift += b;
     }
-    if (__any_sync(kFull, redo != 0)) {
-      // re-linearise the affected particles with exact division where the
-      // certificate failed (identical result wherever it held)
+    if (__any_sync(kFull, redo != 0) && redo) {
+      // re-linearise all four particles of this thread with exact division
+      // (identical wherever the certificate held): the fast path's seg / off
+      // are then dead in this branch and need not survive the calls
 #pragma unroll
       for (int k = 0; k < kItems; ++k) {
-        if (!(redo & (1u << k))) continue;
         const uint64_t so = redo_exact<D, T>(x[0][k], D > 1 ? x[D > 1 ? 1 : 0][k] : T(0),
                                              D > 2 ? x[D > 2 ? 2 : 0][k] : T(0), rec);
         seg[k] = (uint32_t)(so >> 32);
