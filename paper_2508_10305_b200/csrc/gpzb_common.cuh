@@ -218,11 +218,14 @@ __device__ __forceinline__ void block_or(uint32_t (&v)[NV], uint32_t* ws /* kWar
 template <int NV>
 __device__ __forceinline__ void block_or_z(uint32_t (&v)[NV], uint32_t* ws) {
   const int lane = threadIdx.x & 31;
+  // lane i (< NV) ORs the warp's value i: one RED instruction per warp
+  uint32_t mine = 0;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const uint32_t r = __reduce_or_sync(kFull, v[i]);
-    red_or_shared_if(lane == 0 && r, &ws[i], r);
+    mine = lane == i ? r : mine;
   }
+  red_or_shared_if(lane < NV && mine != 0, &ws[lane < NV ? lane : 0], mine);
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < NV; ++i) v[i] = ws[i];
