@@ -81,15 +81,57 @@ def checksum(axes) -> str:
 
 # ------------------------------------------------------------------ clocks
 class Clocks:
+    """SM clock and throttle reasons sampled DURING the timed region: NVML in
+    a sampling thread (every 5 ms, so short regions still get samples), else
+    an `nvidia-smi -lms 50` subprocess."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.nvml = None
+        self.summary = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_sm = float(pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM))
+            self.bits = [getattr(pynvml, "nvmlClocksThrottleReason" + n, d) for n, d in
+                         (("HwSlowdown", 0x8), ("HwThermalSlowdown", 0x40), ("SwThermalSlowdown", 0x20),
+                          ("SwPowerCap", 0x4))]
+            self.nvml = pynvml
+        except Exception:  # noqa: BLE001 - no NVML: fall back to nvidia-smi
+            self.nvml = None
+
+    def _sample(self):
+        import time as _t
+
+        nv = self.nvml
+        while not self.stop.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.handle)
+                for nm, b in zip(self.NAMES, self.bits):
+                    if r & b:
+                        self.reasons.add(nm)
+            except Exception:  # noqa: BLE001
+                return
+            _t.sleep(0.005)
 
     def __enter__(self):
+        if self.nvml is not None:
+            import threading
+
+            self.sm, self.reasons = [], set()
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._sample, daemon=True)
+            self.thread.start()
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
@@ -99,13 +141,19 @@ class Clocks:
         return self
 
     def __exit__(self, *exc):
+        if self.nvml is not None:
+            self.stop.set()
+            self.thread.join(timeout=5)
+            sm = self.sm
+            self.summary = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_sm or None,
+                            "samples": len(sm), "reasons": sorted(self.reasons), "source": "nvml"}
+            return
         if self.proc is None:
             self.summary = None
             return
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
             if len(f) < 8:
@@ -115,11 +163,11 @@ class Clocks:
                 mx = max(mx, float(f[1]))
             except ValueError:
                 continue
-            for nm, v in zip(names, f[4:8]):
+            for nm, v in zip(self.NAMES, f[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         self.summary = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                        "samples": len(sm), "reasons": sorted(reasons)}
+                        "samples": len(sm), "reasons": sorted(reasons), "source": "nvidia-smi"}
 
 
 # ------------------------------------------------------------------ CPU side
