@@ -115,3 +115,48 @@ def test_streamed_errors_match_one_shot(blob):
         e_stream = _err(lambda: gz.decompress(c))
         e_dev = _err(lambda: _one_shot(c))
         assert e_stream is not None and e_stream == e_dev, (e_stream, e_dev)
+
+
+def test_range_decode_any_order_matches_one_shot(blob):
+    """gpzb_decompress_range_async (include/gpzb.h): ranges of one container,
+    issued in any order on one stream, give the one-shot result and outcome."""
+    import ctypes
+
+    from paper_2508_10305_b200 import _lib
+    from paper_2508_10305_b200._lib import lib
+
+    cases = [blob]
+    b = bytearray(blob)
+    h = P.parse_header(blob[:46], len(blob))
+    s0, _ = _block_span(blob, h.block_count // 2)
+    b[s0: s0 + 4] = (7).to_bytes(4, "little")  # a bad count in a middle block
+    cases.append(bytes(b))
+    for data in cases:
+        t = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+        h = P.parse_header(data[:46], len(data))
+        n = h.particle_count
+        outs = [torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(h.dims)]
+        wsb = ctypes.c_uint64()
+        assert lib.gpzb_decompress_workspace(ctypes.byref(h), ctypes.byref(wsb)) == 0
+        ws = torch.empty(wsb.value, dtype=torch.uint8, device="cuda")
+        stream = torch.cuda.current_stream().cuda_stream
+        nb = h.block_count
+        cuts = [0, nb // 5, nb // 2, nb - 3, nb]
+        ranges = list(zip(cuts[:-1], cuts[1:]))[::-1]  # last range first
+        for i, (b0, b1) in enumerate(ranges):
+            st = lib.gpzb_decompress_range_async(t.data_ptr(), t.numel(), ctypes.byref(h),
+                                                 _lib.ptr_array([o.data_ptr() for o in outs]), n, None,
+                                                 ws.data_ptr(), ws.numel(), b0, b1, int(i == 0), stream)
+            assert st == 0
+        res = _lib.Result()
+        lib.gpzb_decompress_result(ws.data_ptr(), ws.numel(), ctypes.byref(h), stream, ctypes.byref(res))
+        err = _err(lambda: _one_shot(data))
+        if err is None:
+            assert res.status == 0
+            want = _one_shot(data)
+            for a in range(h.dims):
+                assert torch.equal(outs[a], want.axes[a])
+        else:
+            assert res.status != 0
+            got = _err(lambda: P._check(res.status, res))
+            assert got == err, (got, err)
