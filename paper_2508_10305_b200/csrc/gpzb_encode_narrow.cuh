@@ -176,14 +176,18 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
   // ---- 3. stream widths (width_for == bit length of the OR) and payload size
   // this thread's runs p0..p0+3 are also the ones it packs in step 5: keep
   // each run's delta | count << 16 (delta < 2^16, count <= 1024) in registers
+  // (vector loads: counts p0..p0+3 in one 16-byte word, ids p0..p0+4 in an
+  // 8-byte word + one; runs >= U are masked, no branches)
   uint32_t dc[kItems], csum = 0, c_or = 0, d_or = 0;
+  {
+    const uint4 c4 = reinterpret_cast<const uint4*>(sm.cnt)[tid];
+    const uint2 u4 = reinterpret_cast<const uint2*>(sm.uniqp)[tid];
+    const uint32_t u[5] = {u4.x & 0xffffu, u4.x >> 16, u4.y & 0xffffu, u4.y >> 16, (uint32_t)sm.uniqp[p0 + 4]};
+    const uint32_t cc[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const uint32_t r = p0 + j;
-    dc[j] = 0;
-    if (r < U) {
-      const uint32_t c = sm.cnt[r];
-      const uint32_t d = (uint32_t)sm.uniqp[r + 1] - (uint32_t)sm.uniqp[r];
+    for (int j = 0; j < kItems; ++j) {
+      const bool in = (uint32_t)(p0 + j) < U;
+      const uint32_t c = in ? cc[j] : 0u, d = in ? u[j + 1] - u[j] : 0u;
       c_or |= c;
       d_or |= d;
       csum += c;
