@@ -217,10 +217,9 @@ __device__ __forceinline__ void narrow_body(const EncParams& P, NarrowSmem& sm, 
         reinterpret_cast<uint4*>(gm)[w] = make_uint4(0, 0, 0, 0);
       uint32_t tot;
       uint32_t ex = block_excl_scan<uint32_t>(csum, tot, sm.scan32);  // its barriers order the zeroing
-#pragma unroll
-      for (int j = 0; j < kItems; ++j) {
-        if (p0 + j < (int)U) sm.u.g.segstart[p0 + j] = (uint16_t)ex;
-        ex += dc[j] >> 16;
+      {  // the four run starts in one 8-byte store (entries past U are never read)
+        const uint32_t e0 = ex, e1 = e0 + (dc[0] >> 16), e2 = e1 + (dc[1] >> 16), e3 = e2 + (dc[2] >> 16);
+        if (p0 < (int)U) reinterpret_cast<uint2*>(sm.u.g.segstart)[tid] = make_uint2(e0 | (e1 << 16), e2 | (e3 << 16));
       }
       uint32_t code[kItems];
 #pragma unroll
