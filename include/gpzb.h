@@ -47,6 +47,8 @@ extern "C" {
 #define GPZB_CORRUPT_DATA 3
 #define GPZB_UNSUPPORTED 4
 #define GPZB_INVALID_ARGUMENT 5
+#define GPZB_NEED_SIDE 6       /* gpzb_compress_result: general-encoder blocks need a side buffer
+                                  of gpzb_result.side_bytes; grow it and encode again */
 #define GPZB_CUDA_ERROR 100
 
 #define GPZB_F32 0          /* model.Precision codes (model.py:29-31) */
@@ -72,7 +74,8 @@ typedef struct gpzb_result {
   int64_t count_block;     /* first block whose particle count breaks the boundary math, or -1 */
   uint32_t table_flags;    /* bit0 start!=0, bit1 not nondecreasing, bit2 end!=payload */
   uint32_t pad_;
-  uint64_t path_blocks[6]; /* reserved (see gpzb_encode_path_counts) */
+  uint64_t side_bytes;     /* compress: side-buffer bytes the general-encoder blocks reserved */
+  uint64_t reserved[5];
 } gpzb_result;
 
 typedef struct gpzb_header {   /* GlobalHeader, container.py:84-95 */
@@ -127,49 +130,78 @@ int gpzb_encode_plan_async(const void* const* axes, int dims, int precision, uin
                            int eb_mode, uint32_t block_size, uint32_t target_segs_per_axis,
                            int preserve_order, void* ws, uint64_t ws_bytes, void* stream);
 
-/* Synchronise and read how many bytes of side buffer the general-encoder
- * blocks need (0 when every block takes the fast path). */
-int gpzb_encode_side_bytes(void* ws, uint64_t ws_bytes, void* stream, uint64_t* side_bytes);
-
-/* Synchronise and read K1.5's routing: side-buffer bytes for the general
- * encoder, and how many narrow blocks go to the CTA encoder (K2) and to the
- * warp encoder (K2p, offset-free blocks).  The counts size the K2 launches. */
-int gpzb_encode_plan_counts(void* ws, uint64_t ws_bytes, void* stream, uint64_t* side_bytes,
-                            uint64_t* cta_blocks, uint64_t* warp_blocks);
-
-/* K2w (general blocks, into `side`) + K2 / K2p (narrow blocks into staging
- * slots) + K3 (look-back scan of the payload lengths, offset table, payload
- * moves), enqueued.  Writes the full container (global header, offset
- * table, payloads) into `out` (capacity from gpzb_compress_bound).
+/* The encoders and K3, enqueued after gpzb_encode_plan_async with no host
+ * synchronisation in between: K2w (general blocks, into `side`), K2s / K2p /
+ * K2 (32-bit fast blocks, into staging slots; every encoder is a persistent
+ * kernel that reads its block list length from the device), then K3
+ * (look-back scan of the payload lengths, offset table, payload moves).
+ * Writes the full container (global header, offset table, payloads) into
+ * `out` (capacity from gpzb_compress_bound).
+ *   side / side_cap: buffer for the payloads of general-encoder blocks (may
+ *   be NULL / 0).  If those blocks need more, nothing of theirs is written
+ *   and gpzb_compress_result returns GPZB_NEED_SIDE with the exact size in
+ *   gpzb_result.side_bytes; the caller grows the buffer and runs reset +
+ *   range + plan + encode again.  Blocks take the general encoder only
+ *   outside the fast path's envelope (preserve_order, > 32-bit keys,
+ *   Π N > 2^16, half-bound axes).
  *   table_base / header_count / header_blocks: sharding hooks — table entries
  *   are written as table_base + local prefix, and the global header (written
  *   when write_header != 0) names header_count particles in header_blocks
- *   blocks.  Single-GPU callers pass 0, count, ceil(count/bs), 1.
- *   cta_blocks / warp_blocks: from gpzb_encode_plan_counts (UINT64_MAX for
- *   both: unknown, every encoder is launched over all blocks). */
+ *   blocks.  Single-GPU callers pass 0, count, ceil(count/bs), 1. */
 int gpzb_encode_async(const void* const* axes, int dims, int precision, uint64_t count, double eb,
                       int eb_mode, uint32_t block_size, uint32_t target_segs_per_axis,
                       int preserve_order, void* ws, uint64_t ws_bytes, uint8_t* side,
-                      uint64_t side_bytes, uint8_t* out, uint64_t out_cap, uint64_t table_base,
-                      uint64_t header_count, uint64_t header_blocks, int write_header,
-                      uint64_t cta_blocks, uint64_t warp_blocks, void* stream);
+                      uint64_t side_cap, uint8_t* out, uint64_t out_cap, uint64_t table_base,
+                      uint64_t header_count, uint64_t header_blocks, int write_header, void* stream);
 
 /* Synchronise `stream` and read the result record of the last encode. */
 int gpzb_compress_result(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t block_size,
                          void* stream, gpzb_result* res);
 
-/* Convenience: reset + range + plan + encode + result, one call (allocates
- * the side buffer with cudaMallocAsync when general-path blocks exist). */
+/* Convenience: reset + range + plan + encode + result, one call.  A second
+ * pass with a cudaMallocAsync'd side buffer runs only when general-encoder
+ * blocks exist. */
 int gpzb_compress(const void* const* axes, int dims, int precision, uint64_t count, double eb,
                   int eb_mode, uint32_t block_size, uint32_t target_segs_per_axis,
                   int preserve_order, void* ws, uint64_t ws_bytes, uint8_t* out,
                   uint64_t out_cap, void* stream, gpzb_result* res);
 
-/* Diagnostics: blocks of the last compression in `ws` per offset-order path
- * (0 no offsets, 1 composite bitmap, 2 in-group compare, 3 LSD, 4 general
- * encoder, 5 group masks or general with ranks).  Synchronous. */
+/* Diagnostics: blocks of the last compression in `ws` per encoder path,
+ * counts[8]: 0 no offsets (K2, K2p), 1 composite bitmap, 2 in-group compare,
+ * 3 LSD, 4 general encoder, 5 group masks or general with ranks, 6 K2s with
+ * offsets, 7 K2s without offsets.  Synchronous. */
 int gpzb_encode_path_counts(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t block_size, int dims,
                             int precision, void* stream, uint64_t* counts);
+
+/* ---- stage-level entry points (per-stage parity; the compress path fuses
+ *      these stages into its own kernels) ---------------------------------- */
+
+/* quantizer.block_bounds + derive_geometry (quantizer.py:51-129) for every
+ * block: lohi[(blk*dims + a)*2 + {0,1}] = the block's min / max of axis a
+ * (exact, as float64), Q / N = bins and segments per axis, log2m = log2 of
+ * the segment size.  Any output may be NULL.  ws: gpzb_compress_workspace.
+ * Synchronous; errors as in compression (non-finite input: DomainError with
+ * the axis; the first failing block's WidthOverflow / DomainError). */
+int gpzb_block_geometry(const void* const* axes, int dims, int precision, uint64_t count, uint32_t block_size,
+                        uint32_t target_segs_per_axis, double eb_abs, double* lohi, uint64_t* Q, uint64_t* N,
+                        uint8_t* log2m, void* ws, uint64_t ws_bytes, void* stream, gpzb_result* res);
+
+/* quantizer.quantize_block (quantizer.py:223-247): the linearised
+ * (seg_id, offset) of every particle, in input order, as u64 (seg and off:
+ * `count` each).  lohi: NULL to use each block's own bounds, or carried
+ * bounds in gpzb_block_geometry's layout (the geometry of another dataset,
+ * as metrics.pair_blocks and the code fixed point use).  ws:
+ * gpzb_compress_workspace.  Synchronous. */
+int gpzb_quantize(const void* const* axes, int dims, int precision, uint64_t count, uint32_t block_size,
+                  uint32_t target_segs_per_axis, double eb_abs, const double* lohi, uint64_t* seg, uint64_t* off,
+                  void* ws, uint64_t ws_bytes, void* stream, gpzb_result* res);
+
+/* container.compact's offsets (container.py:203-208): offsets[0] = 0,
+ * offsets[i + 1] = offsets[i] + sizes[i] (u64, device arrays, nblocks + 1
+ * outputs) by the K3a decoupled look-back scan.  Enqueued. */
+int gpzb_scan_workspace(uint64_t nblocks, uint64_t* ws_bytes);
+int gpzb_scan_sizes(const uint64_t* sizes, uint64_t nblocks, uint64_t* offsets, void* ws, uint64_t ws_bytes,
+                    void* stream);
 
 /* ---- decompression ------------------------------------------------------ */
 

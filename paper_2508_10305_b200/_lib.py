@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GPZB_LIB") or os.path.join(_HERE, "_gpzb.so")  # GPZB_LIB: A/B builds
 
-OK, DOMAIN, WIDTH, CORRUPT, UNSUPPORTED, INVALID = 0, 1, 2, 3, 4, 5
+OK, DOMAIN, WIDTH, CORRUPT, UNSUPPORTED, INVALID, NEED_SIDE = 0, 1, 2, 3, 4, 5, 6
 F32, F64 = 0, 1
 GLOBAL_HEADER_SIZE = 46
 MAX_BLOCK_SIZE = 1024
@@ -33,7 +33,8 @@ class Result(ctypes.Structure):
         ("count_block", ctypes.c_int64),
         ("table_flags", ctypes.c_uint32),
         ("pad_", ctypes.c_uint32),
-        ("path_blocks", ctypes.c_uint64 * 6),
+        ("side_bytes", ctypes.c_uint64),
+        ("reserved", ctypes.c_uint64 * 5),
     ]
 
 
@@ -67,14 +68,17 @@ SIGNATURES = {
     "gpzb_range_words": (_I32, [_VP, _U64, ctypes.POINTER(_VP)]),
     "gpzb_encode_plan_async": (_I32, [ctypes.POINTER(_VP), _I32, _I32, _U64, _D, _I32, _U32, _U32, _I32, _VP,
                                       _U64, _VP]),
-    "gpzb_encode_side_bytes": (_I32, [_VP, _U64, _VP, ctypes.POINTER(_U64)]),
-    "gpzb_encode_plan_counts": (_I32, [_VP, _U64, _VP, ctypes.POINTER(_U64), ctypes.POINTER(_U64),
-                                       ctypes.POINTER(_U64)]),
     "gpzb_encode_async": (_I32, [ctypes.POINTER(_VP), _I32, _I32, _U64, _D, _I32, _U32, _U32, _I32, _VP, _U64,
-                                 _VP, _U64, _VP, _U64, _U64, _U64, _U64, _I32, _U64, _U64, _VP]),
+                                 _VP, _U64, _VP, _U64, _U64, _U64, _U64, _I32, _VP]),
     "gpzb_compress_result": (_I32, [_VP, _U64, _U64, _U32, _VP, _RES]),
     "gpzb_compress": (_I32, [ctypes.POINTER(_VP), _I32, _I32, _U64, _D, _I32, _U32, _U32, _I32, _VP, _U64, _VP,
                              _U64, _VP, _RES]),
+    "gpzb_block_geometry": (_I32, [ctypes.POINTER(_VP), _I32, _I32, _U64, _U32, _U32, _D, _VP, _VP, _VP, _VP, _VP,
+                                   _U64, _VP, _RES]),
+    "gpzb_quantize": (_I32, [ctypes.POINTER(_VP), _I32, _I32, _U64, _U32, _U32, _D, _VP, _VP, _VP, _VP, _U64, _VP,
+                             _RES]),
+    "gpzb_scan_workspace": (_I32, [_U64, ctypes.POINTER(_U64)]),
+    "gpzb_scan_sizes": (_I32, [_VP, _U64, _VP, _VP, _U64, _VP]),
     "gpzb_parse_header": (_I32, [ctypes.c_char_p, _U64, _U64, _HDR, _RES]),
     "gpzb_block_counts_async": (_I32, [_VP, _U64, _HDR, _VP, _VP]),
     "gpzb_decompress": (_I32, [_VP, _U64, _HDR, ctypes.POINTER(_VP), _U64, _VP, _VP, _U64, _VP, _RES]),

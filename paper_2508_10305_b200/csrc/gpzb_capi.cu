@@ -7,14 +7,19 @@
 #include <cstdio>
 #include <cstring>
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "gpzb_decode.cuh"
 #include "gpzb_decode_warp.cuh"
 #include "gpzb_encode.cuh"
 #include "gpzb_encode_narrow.cuh"
+#include "gpzb_encode_small.cuh"
 #include "gpzb_encode_warp.cuh"
 #include "gpzb_encode_wide.cuh"
 #include "gpzb_metrics.cuh"
+#include "gpzb_stages.cuh"
 
 using namespace gpzb;
 
@@ -32,7 +37,7 @@ std::atomic<unsigned long long> g_launches{0};
 inline uint64_t align_up(uint64_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
 
 struct EncLayout {
-  uint64_t status, tstat, bounds, rec, list, ctalist, staging, total;
+  uint64_t status, tstat, bounds, rec, list, ctalist, slist, staging, total;
 };
 
 inline uint64_t nblocks_of(uint64_t count, uint32_t bs) { return bs ? (count + bs - 1) / bs : 0; }
@@ -45,7 +50,8 @@ EncLayout enc_layout(uint64_t nblocks, int dims, int prec) {
   L.rec = align_up(L.bounds + nblocks * 2ull * dims * (prec ? 8 : 4));
   L.list = align_up(L.rec + nblocks * sizeof(BlkRec));
   L.ctalist = align_up(L.list + 4 * nblocks);
-  L.staging = align_up(L.ctalist + 4 * nblocks);
+  L.slist = align_up(L.ctalist + 4 * nblocks);
+  L.staging = align_up(L.slist + 4 * nblocks);
   L.total = align_up(L.staging + (uint64_t)kSlotBytes * nblocks);
   return L;
 }
@@ -54,6 +60,27 @@ int sm_count() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   return n > 0 ? n : 148;
+}
+
+// Per-device launch facts, cached per (kernel, device): the dynamic
+// shared-memory opt-in is a per-device function attribute, and the occupancy
+// query sizes the persistent grids.
+std::mutex g_attr_mu;
+std::map<std::tuple<const void*, int, int, size_t>, int> g_occ;
+
+template <typename K>
+int occupancy(K kern, int threads, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kern), dev, threads, smem);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  auto it = g_occ.find(key);
+  if (it != g_occ.end()) return it->second;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem) != cudaSuccess || per < 1) per = 1;
+  g_occ[key] = per;
+  return per;
 }
 
 inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? GPZB_OK : GPZB_CUDA_ERROR + (int)e; }
@@ -120,38 +147,33 @@ void launch_geometry(const EncParams& P, cudaStream_t s) {
 }
 
 template <int D, bool F64>
-void launch_encode(const EncParams& P, bool wide, uint64_t cta_blocks, uint64_t warp_blocks, cudaStream_t s) {
-  if (wide) {
+void launch_encode(const EncParams& P, cudaStream_t s) {
+  {  // K2w: persistent over K1.5's list of general blocks (usually empty)
     const unsigned grid = (unsigned)std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * 4);
     if (P.preserve) { GPZB_COUNT_LAUNCH(); k_encode_wide<D, F64, true><<<grid, kThreads, 0, s>>>(P); }
     else { GPZB_COUNT_LAUNCH(); k_encode_wide<D, F64, false><<<grid, kThreads, 0, s>>>(P); }
   }
-  // K2 (CTA encoder): launch-order blocks when no block went to the warp
-  // encoder, else exactly the listed blocks; K2p (warp encoder) when any
-  // block is offset-free (counts from gpzb_encode_plan_counts; ~0 = unknown)
-  const bool known = cta_blocks != ~0ull && warp_blocks != ~0ull;
-  if (!known || cta_blocks > 0) {
-    EncParams Q = P;
-    Q.cta_mode = (known && warp_blocks == 0) ? 0 : 1;
-    const uint64_t grid = Q.cta_mode ? (known ? cta_blocks : P.nblocks) : P.nblocks;
-    if (!known) Q.cta_mode = 2;  // grid over all blocks, entries past the count exit
+  // K2s first (it may hand blocks back to K2's list), then K2p and K2; every
+  // encoder is persistent and reads its block count on the device
+  if constexpr (!F64) {
+    const uint64_t sm = (uint64_t)sm_count();
+    const unsigned g1 = (unsigned)std::min<uint64_t>(P.nblocks, sm * occupancy(k_encode_small<D, true>, kST, 0));
+    const unsigned g0 = (unsigned)std::min<uint64_t>(P.nblocks, sm * occupancy(k_encode_small<D, false>, kST, 0));
     GPZB_COUNT_LAUNCH();
-    k_encode<D, F64><<<(unsigned)grid, kThreads, 0, s>>>(Q);
+    k_encode_small<D, true><<<g1, kST, 0, s>>>(P);
+    GPZB_COUNT_LAUNCH();
+    k_encode_small<D, false><<<g0, kST, 0, s>>>(P);
   }
-  if (!known || warp_blocks > 0) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_encode_warp<D, F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kWarpEncSmemBytes);
-      attr = true;
-    }
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_encode_warp<D, F64>, 32 * kWarpEncWarps,
-                                                  kWarpEncSmemBytes);
+  if (!P.small0 || F64) {
     const unsigned wgrid = (unsigned)std::min<uint64_t>((P.nblocks + kWarpEncWarps - 1) / kWarpEncWarps,
-                                                        (uint64_t)sm_count() * std::max(per_sm, 1));
+                                                        (uint64_t)sm_count() * occupancy(k_encode_warp<D, F64>, 32 * kWarpEncWarps, kWarpEncSmemBytes));
     GPZB_COUNT_LAUNCH();
     k_encode_warp<D, F64><<<wgrid, 32 * kWarpEncWarps, kWarpEncSmemBytes, s>>>(P);
+  }
+  {
+    const unsigned cgrid = (unsigned)std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * occupancy(k_encode<D, F64>, kThreads, 0));
+    GPZB_COUNT_LAUNCH();
+    k_encode<D, F64><<<cgrid, kThreads, 0, s>>>(P);
   }
   // K3: scan of the payload lengths, offset table, payload moves
   CompactParams C;
@@ -194,17 +216,9 @@ void launch_decode(const DecParams& P, bool pres, cudaStream_t s) {
   } else {
     GPZB_COUNT_LAUNCH();
     k_decode_plan<D, F64, false><<<pgrid, 256, 0, s>>>(P);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_decode_warp<D, F64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kWarpDecSmemBytes);
-      attr = true;
-    }
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_decode_warp<D, F64>, 32 * kWarpDecWarps,
-                                                  kWarpDecSmemBytes);
+    const int per_sm = occupancy(k_decode_warp<D, F64>, 32 * kWarpDecWarps, kWarpDecSmemBytes);
     const unsigned wgrid = (unsigned)std::min<uint64_t>((nb + kWarpDecWarps - 1) / kWarpDecWarps,
-                                                        (uint64_t)sm_count() * std::max(per_sm, 1));
+                                                        (uint64_t)sm_count() * per_sm);
     GPZB_COUNT_LAUNCH();
     k_decode_warp<D, F64><<<wgrid, 32 * kWarpDecWarps, kWarpDecSmemBytes, s>>>(P);
     GPZB_COUNT_LAUNCH();
@@ -281,12 +295,135 @@ EncParams make_enc(const void* const* axes, int dims, int prec, uint64_t count, 
   P.rec = reinterpret_cast<BlkRec*>(static_cast<uint8_t*>(ws) + L.rec);
   P.wide_list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + L.list);
   P.cta_list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + L.ctalist);
+  P.small_list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + L.slist);
+  // routing switches (diagnostics / A-B runs): GPZB_ROUTE=cta sends every
+  // narrow block to the general CTA encoder K2, GPZB_ROUTE=small0 sends the
+  // offset-free full f32 blocks to K2s instead of the warp encoder K2p
+  const char* route = getenv("GPZB_ROUTE");
+  P.use_small = !(route && strcmp(route, "cta") == 0);
+  P.small0 = route && strcmp(route, "small0") == 0;
   return P;
+}
+
+template <int D, bool F64>
+void launch_stage_geometry(const EncParams& P, const double* lohi_in, double eb_abs, uint32_t target, AxisGeo* geo,
+                           double* lohi, uint64_t* Q, uint64_t* N, uint8_t* bits, cudaStream_t s) {
+  using T = typename std::conditional<F64, double, float>::type;
+  const unsigned grid = (unsigned)((P.nblocks + 255) / 256);
+  GPZB_COUNT_LAUNCH();
+  if (lohi_in)
+    k_stage_geometry<D, double><<<grid, 256, 0, s>>>(lohi_in, P.nblocks, eb_abs, target, F64, geo, lohi, Q, N, bits, P.res);
+  else
+    k_stage_geometry<D, T><<<grid, 256, 0, s>>>(reinterpret_cast<const T*>(P.bounds), P.nblocks, eb_abs, target, F64,
+                                                geo, lohi, Q, N, bits, P.res);
+}
+
+template <int D, bool F64>
+void launch_stage_quantize(const EncParams& P, const AxisGeo* geo, double eb_abs, uint64_t* seg, uint64_t* off,
+                           cudaStream_t s) {
+  using T = typename std::conditional<F64, double, float>::type;
+  GPZB_COUNT_LAUNCH();
+  k_stage_quantize<D, T><<<(unsigned)((P.count + 255) / 256), 256, 0, s>>>(P, geo, eb_abs, seg, off);
+}
+
+// Shared tail of the stage entry points: synchronise, then report the
+// dataset-level finiteness error first, then the first failing block.
+int stage_result(void* ws, cudaStream_t s, gpzb_result* res) {
+  DevResult R;
+  cudaError_t e = cudaMemcpyAsync(&R, ws, sizeof(R), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return res->status = cuda_status(e);
+  res->nonfinite_mask = R.nonfinite_mask;
+  if (R.nonfinite_mask) {
+    res->reason = R_NONFINITE;
+    res->axis = __builtin_ctz(R.nonfinite_mask);
+    return res->status = GPZB_DOMAIN_ERROR;
+  }
+  if (R.err_block) {
+    decode_err(R.err_block, &res->block, &res->axis, &res->reason);
+    return res->status = status_of_reason(res->reason);
+  }
+  return GPZB_OK;
 }
 
 }  // namespace
 
 extern "C" {
+
+int gpzb_block_geometry(const void* const* axes, int dims, int prec, uint64_t count, uint32_t bs, uint32_t target,
+                        double eb_abs, double* lohi, uint64_t* Q, uint64_t* N, uint8_t* log2m, void* ws,
+                        uint64_t ws_bytes, void* stream, gpzb_result* res) {
+  clear_result(res);
+  int st = check_args(dims, prec, bs);
+  if (st) return res->status = st;
+  if (target == 0 || (target & (target - 1))) return res->status = GPZB_INVALID_ARGUMENT;
+  const uint64_t nb = nblocks_of(count, bs);
+  const EncLayout L = enc_layout(nb, dims, prec);
+  if (ws_bytes < L.total) return res->status = GPZB_INVALID_ARGUMENT;
+  if (nb == 0) return GPZB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  st = gpzb_workspace_reset_async(ws, ws_bytes, count, bs, stream);
+  if (st) return res->status = st;
+  EncParams P = make_enc(axes, dims, prec, count, bs, ws);
+  DISPATCH_DP(dims, prec, launch_range, P, s);  // per-block bounds + finiteness (block_bounds)
+  DISPATCH_DP(dims, prec, launch_stage_geometry, P, nullptr, eb_abs, target, nullptr, lohi, Q, N, log2m, s);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return res->status = cuda_status(e);
+  return stage_result(ws, s, res);
+}
+
+int gpzb_quantize(const void* const* axes, int dims, int prec, uint64_t count, uint32_t bs, uint32_t target,
+                  double eb_abs, const double* lohi, uint64_t* seg, uint64_t* off, void* ws, uint64_t ws_bytes,
+                  void* stream, gpzb_result* res) {
+  clear_result(res);
+  int st = check_args(dims, prec, bs);
+  if (st) return res->status = st;
+  if (target == 0 || (target & (target - 1))) return res->status = GPZB_INVALID_ARGUMENT;
+  const uint64_t nb = nblocks_of(count, bs);
+  const EncLayout L = enc_layout(nb, dims, prec);
+  if (ws_bytes < L.total) return res->status = GPZB_INVALID_ARGUMENT;
+  if (nb == 0) return GPZB_OK;
+  static_assert(3 * sizeof(AxisGeo) <= kSlotBytes, "geometry records fit the staging slots");
+  cudaStream_t s = (cudaStream_t)stream;
+  st = gpzb_workspace_reset_async(ws, ws_bytes, count, bs, stream);
+  if (st) return res->status = st;
+  EncParams P = make_enc(axes, dims, prec, count, bs, ws);
+  AxisGeo* geo = reinterpret_cast<AxisGeo*>(static_cast<uint8_t*>(ws) + L.staging);
+  if (!lohi) DISPATCH_DP(dims, prec, launch_range, P, s);  // the block's own bounds
+  DISPATCH_DP(dims, prec, launch_stage_geometry, P, lohi, eb_abs, target, geo, nullptr, nullptr, nullptr, nullptr, s);
+  DISPATCH_DP(dims, prec, launch_stage_quantize, P, geo, eb_abs, seg, off, s);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return res->status = cuda_status(e);
+  return stage_result(ws, s, res);
+}
+
+int gpzb_scan_workspace(uint64_t nblocks, uint64_t* ws_bytes) {
+  *ws_bytes = enc_layout(nblocks, 1, 0).bounds;
+  return GPZB_OK;
+}
+
+int gpzb_scan_sizes(const uint64_t* sizes, uint64_t nblocks, uint64_t* offsets, void* ws, uint64_t ws_bytes,
+                    void* stream) {
+  const EncLayout L = enc_layout(nblocks, 1, 0);
+  if (ws_bytes < L.bounds) return GPZB_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(ws, 0, L.bounds, s);
+  unsigned long long* sz = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(ws) + L.status);
+  if (e == cudaSuccess && nblocks) e = cudaMemcpyAsync(sz, sizes, 8 * nblocks, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (nblocks == 0) return cuda_status(cudaMemsetAsync(offsets, 0, 8, s));
+  CompactParams C;
+  memset(&C, 0, sizeof(C));
+  C.sizes = sz;
+  C.tstat = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(ws) + L.tstat);
+  C.nblocks = nblocks;
+  C.table0 = reinterpret_cast<uint8_t*>(offsets);
+  C.table = reinterpret_cast<uint8_t*>(offsets + 1);
+  C.res = reinterpret_cast<DevResult*>(ws);
+  GPZB_COUNT_LAUNCH();
+  k_scan_sizes<<<(unsigned)((nblocks + kScanTile - 1) / kScanTile), kScanThreads, 0, s>>>(C);
+  return cuda_status(cudaGetLastError());
+}
 
 const char* gpzb_version(void) { return "gpzb 0.1 sm_100a"; }
 
@@ -412,34 +549,10 @@ int gpzb_encode_plan_async(const void* const* axes, int dims, int prec, uint64_t
   return cuda_status(cudaGetLastError());
 }
 
-int gpzb_encode_side_bytes(void* ws, uint64_t ws_bytes, void* stream, uint64_t* side_bytes) {
-  if (ws_bytes < sizeof(DevResult)) return GPZB_INVALID_ARGUMENT;
-  unsigned long long v = 0;
-  cudaError_t e = cudaMemcpyAsync(&v, &reinterpret_cast<DevResult*>(ws)->side_bytes, 8, cudaMemcpyDeviceToHost,
-                                  (cudaStream_t)stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
-  *side_bytes = v;
-  return cuda_status(e);
-}
-
-int gpzb_encode_plan_counts(void* ws, uint64_t ws_bytes, void* stream, uint64_t* side_bytes,
-                            uint64_t* cta_blocks, uint64_t* warp_blocks) {
-  if (ws_bytes < sizeof(DevResult)) return GPZB_INVALID_ARGUMENT;
-  DevResult R;
-  cudaError_t e = cudaMemcpyAsync(&R, ws, sizeof(R), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
-  if (e != cudaSuccess) return cuda_status(e);
-  *side_bytes = R.side_bytes;
-  *cta_blocks = R.cta_count;
-  *warp_blocks = R.warp_count;
-  return GPZB_OK;
-}
-
 int gpzb_encode_async(const void* const* axes, int dims, int prec, uint64_t count, double eb, int eb_mode,
                       uint32_t bs, uint32_t target, int pres, void* ws, uint64_t ws_bytes, uint8_t* side,
-                      uint64_t side_bytes, uint8_t* out, uint64_t out_cap, uint64_t table_base,
-                      uint64_t header_count, uint64_t header_blocks, int write_header, uint64_t cta_blocks,
-                      uint64_t warp_blocks, void* stream) {
+                      uint64_t side_cap, uint8_t* out, uint64_t out_cap, uint64_t table_base,
+                      uint64_t header_count, uint64_t header_blocks, int write_header, void* stream) {
   int st = check_args(dims, prec, bs);
   if (st) return st;
   if (target == 0 || (target & (target - 1))) return GPZB_INVALID_ARGUMENT;
@@ -456,6 +569,7 @@ int gpzb_encode_async(const void* const* axes, int dims, int prec, uint64_t coun
   P.eb_mode_code = eb_mode;
   P.preserve = pres != 0;
   P.side = side;
+  P.side_cap = side ? side_cap : 0;
   P.header = write_header ? out : nullptr;
   P.table0 = out + GPZB_GLOBAL_HEADER_SIZE;
   P.table = out + GPZB_GLOBAL_HEADER_SIZE + 8;
@@ -463,7 +577,7 @@ int gpzb_encode_async(const void* const* axes, int dims, int prec, uint64_t coun
   P.table_base = table_base;
   P.header_count = header_count;
   P.header_blocks = header_blocks;
-  DISPATCH_DP(dims, prec, launch_encode, P, side_bytes > 0, cta_blocks, warp_blocks, (cudaStream_t)stream);
+  DISPATCH_DP(dims, prec, launch_encode, P, (cudaStream_t)stream);
   return cuda_status(cudaGetLastError());
 }
 
@@ -478,6 +592,7 @@ int gpzb_compress_result(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t b
   const uint64_t nb = nblocks_of(count, bs);
   res->nonfinite_mask = R.nonfinite_mask;
   res->eb_abs = R.eb_abs;
+  res->side_bytes = R.side_bytes;
   if (R.nonfinite_mask) {  // Dataset construction fails before any block (model.py:75-77)
     res->status = GPZB_DOMAIN_ERROR;
     res->reason = R_NONFINITE;
@@ -487,6 +602,10 @@ int gpzb_compress_result(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t b
   if (R.err_block) {
     decode_err(R.err_block, &res->block, &res->axis, &res->reason);
     res->status = status_of_reason(res->reason);
+    return res->status;
+  }
+  if (R.side_need) {  // general-encoder blocks did not fit the caller's side buffer
+    res->status = GPZB_NEED_SIDE;
     return res->status;
   }
   res->out_len = GPZB_GLOBAL_HEADER_SIZE + 8 * (nb + 1) + R.total_payload;
@@ -501,14 +620,14 @@ int gpzb_encode_path_counts(void* ws, uint64_t ws_bytes, uint64_t count, uint32_
   if (ws_bytes < L.total) return GPZB_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
   unsigned long long* dev = &reinterpret_cast<DevResult*>(ws)->path_blocks[0];
-  cudaError_t e = cudaMemsetAsync(dev, 0, 6 * sizeof(unsigned long long), s);
+  cudaError_t e = cudaMemsetAsync(dev, 0, 8 * sizeof(unsigned long long), s);
   if (e == cudaSuccess && nb) {
     GPZB_COUNT_LAUNCH();
     k_path_counts<<<(unsigned)std::min<uint64_t>((nb + 255) / 256, 1024), 256, 0, s>>>(
         reinterpret_cast<const BlkRec*>(static_cast<uint8_t*>(ws) + L.rec), nb, dev);
     e = cudaGetLastError();
   }
-  if (e == cudaSuccess) e = cudaMemcpyAsync(counts, dev, 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(counts, dev, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   return cuda_status(e);
 }
@@ -543,23 +662,27 @@ int gpzb_compress(const void* const* axes, int dims, int prec, uint64_t count, d
     res->eb_abs = eb;
     return GPZB_OK;
   }
-  st = gpzb_workspace_reset_async(ws, ws_bytes, count, bs, stream);
-  if (!st) st = gpzb_range_async(axes, dims, prec, count, bs, ws, ws_bytes, stream);
-  if (!st) st = gpzb_encode_plan_async(axes, dims, prec, count, eb, eb_mode, bs, target, pres, ws, ws_bytes, stream);
-  uint64_t side_bytes = 0, cta_blocks = ~0ull, warp_blocks = ~0ull;
-  if (!st) st = gpzb_encode_plan_counts(ws, ws_bytes, stream, &side_bytes, &cta_blocks, &warp_blocks);
+  // one pass without a side buffer; general-encoder blocks (rare) report the
+  // bytes they need and the pass is repeated once with a buffer that size
   void* side = nullptr;
-  if (!st && side_bytes) {  // the one allocation of the convenience wrapper (stream-ordered pool)
-    cudaError_t e = cudaMallocAsync(&side, side_bytes, s);
-    if (e != cudaSuccess) st = cuda_status(e);
+  uint64_t side_cap = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    st = gpzb_workspace_reset_async(ws, ws_bytes, count, bs, stream);
+    if (!st) st = gpzb_range_async(axes, dims, prec, count, bs, ws, ws_bytes, stream);
+    if (!st) st = gpzb_encode_plan_async(axes, dims, prec, count, eb, eb_mode, bs, target, pres, ws, ws_bytes, stream);
+    if (!st)
+      st = gpzb_encode_async(axes, dims, prec, count, eb, eb_mode, bs, target, pres, ws, ws_bytes,
+                             static_cast<uint8_t*>(side), side_cap, out, out_cap, 0, count, nb, 1, stream);
+    if (!st) st = gpzb_compress_result(ws, ws_bytes, count, bs, stream, res);
+    if (st != GPZB_NEED_SIDE || pass == 1) break;
+    side_cap = res->side_bytes;
+    cudaError_t e = cudaMallocAsync(&side, side_cap, s);  // the wrapper's one allocation (stream-ordered pool)
+    if (e != cudaSuccess) { st = cuda_status(e); side = nullptr; break; }
   }
-  if (!st)
-    st = gpzb_encode_async(axes, dims, prec, count, eb, eb_mode, bs, target, pres, ws, ws_bytes,
-                           static_cast<uint8_t*>(side), side_bytes, out, out_cap, 0, count, nb, 1, cta_blocks,
-                           warp_blocks, stream);
   if (side) cudaFreeAsync(side, s);
-  if (st) return res->status = st;
-  return gpzb_compress_result(ws, ws_bytes, count, bs, stream, res);
+  if (st == GPZB_NEED_SIDE) st = GPZB_INVALID_ARGUMENT;  // cannot happen: the second pass had the exact size
+  if (st && !res->status) res->status = st;
+  return st;
 }
 
 int gpzb_parse_header(const uint8_t* hb, uint64_t avail, uint64_t len, gpzb_header* h, gpzb_result* res) {

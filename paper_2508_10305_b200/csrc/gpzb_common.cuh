@@ -52,16 +52,18 @@ struct DevResult {
   unsigned long long err_count;     // decompress: count-vs-boundary errors (pipeline.py:174-181)
   unsigned int nonfinite_mask;      // bit a: axis a holds a non-finite value
   unsigned int table_flags;         // bit0 start, bit1 order, bit2 end (container.py:282-290)
-  unsigned long long ticket;        // dynamic block ids for the look-back
+  unsigned long long side_need;     // compress: K2w found the side buffer too small (bytes K1.5 reserved)
   unsigned long long total_payload; // inclusive prefix of the last block
   unsigned long long range_w[2];    // ukey(-lo), ukey(hi): joint range (model.py:194-195)
   double eb_abs;
-  unsigned long long path_blocks[6];
+  unsigned long long path_blocks[8];
   unsigned long long side_bytes;    // K1.5: bytes reserved in the side buffer for wide blocks
   unsigned int wide_count;          // K1.5: number of wide blocks (decode: K4a's CTA-list length)
   unsigned int cta_count;           // K1.5: narrow blocks for the CTA encoder (its list length)
   unsigned int warp_count;          // K1.5: blocks for the warp encoder
-  unsigned int pad_[3];
+  unsigned int small_count;         // K1.5: blocks for K2s with offsets (small_list from the front)
+  unsigned int small0_count;        // K1.5: blocks for K2s without offsets (small_list from the back)
+  unsigned int pad_;
 };
 static_assert(sizeof(DevResult) % 16 == 0, "DevResult alignment");
 

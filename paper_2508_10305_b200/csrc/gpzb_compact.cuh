@@ -214,13 +214,13 @@ __global__ void __launch_bounds__(32 * kCopyWarps) k_copy_payloads(const Compact
 
 // Diagnostics: how many blocks took each offset-order path (BlkRec::path).
 __global__ void k_path_counts(const BlkRec* rec, uint64_t nblocks, unsigned long long* counts) {
-  __shared__ unsigned int h[6];
-  if (threadIdx.x < 6) h[threadIdx.x] = 0;
+  __shared__ unsigned int h[8];
+  if (threadIdx.x < 8) h[threadIdx.x] = 0;
   __syncthreads();
   for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nblocks; b += (uint64_t)gridDim.x * blockDim.x)
-    if (rec[b].kind != KIND_ERROR && rec[b].path < 6) atomicAdd(&h[rec[b].path], 1u);
+    if (rec[b].kind != KIND_ERROR && rec[b].path < 8) atomicAdd(&h[rec[b].path], 1u);
   __syncthreads();
-  if (threadIdx.x < 6 && h[threadIdx.x]) atomicAdd(&counts[threadIdx.x], (unsigned long long)h[threadIdx.x]);
+  if (threadIdx.x < 8 && h[threadIdx.x]) atomicAdd(&counts[threadIdx.x], (unsigned long long)h[threadIdx.x]);
 }
 
 }  // namespace gpzb

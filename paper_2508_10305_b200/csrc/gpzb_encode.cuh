@@ -43,9 +43,12 @@ struct EncParams {
   int preserve;
   BlkRec* rec;             // per-block geometry records (K1.5)
   uint32_t* wide_list;     // blocks routed to the general encoder
-  uint32_t* cta_list;      // narrow blocks for the CTA encoder (the rest of them go to the warp encoder)
-  int cta_mode;            // 0: CTA i encodes block i (every narrow block is a CTA block); 1: CTA i takes cta_list[i]
+  uint32_t* cta_list;      // narrow blocks for the general CTA encoder K2 (K1.5, then K2s hand-backs)
+  uint32_t* small_list;    // K2s blocks: with offsets from the front, offset-free from the back
+  int small0;              // route offset-free full f32 blocks to K2s (1) or to the warp encoder K2p (0)
+  int use_small;           // route blocks to K2s at all (diagnostics switch)
   uint8_t* side;           // staging for the general encoder's payloads
+  uint64_t side_cap;       // its capacity in bytes (K2w reports a shortfall instead of writing past it)
   uint8_t* staging;        // narrow payloads: one kSlotBytes slot per block (K3 concatenates)
 };
 
@@ -350,7 +353,11 @@ struct __align__(16) BlkRec {
 };
 static_assert(sizeof(BlkRec) == 128, "BlkRec layout");
 
-enum : uint8_t { KIND_NARROW = 0, KIND_WIDE = 1, KIND_ERROR = 2, KIND_WARP = 3 };
+enum : uint8_t { KIND_NARROW = 0, KIND_WIDE = 1, KIND_ERROR = 2, KIND_WARP = 3, KIND_SMALL = 4 };
+
+// Full float32 blocks with Σ log2 m <= kSmallMaxSumb (16 nibble counters in
+// one u64 per segment rank) take the K2s encoder (gpzb_encode_small.cuh).
+constexpr uint32_t kSmallMaxSumb = 4;
 
 // Narrow blocks the warp encoder K2p takes: full, vector-loadable, no
 // offset stream (every log2 m == 0) and Π N <= 16384.
@@ -426,12 +433,18 @@ __global__ void __launch_bounds__(256) k_geometry(const EncParams P) {
     rec.sumb = (uint8_t)sumb;
     if (narrow) {
       const uint64_t n = min((uint64_t)P.bs, P.count - blk * (uint64_t)P.bs);
-      if (sumb == 0 && PN <= kWarpEncMaxPN && n == (uint64_t)kMaxBs && P.vec && P.cta_list) {
+      const bool full = n == (uint64_t)kMaxBs && P.vec;
+      if (full && sizeof(T) == 4 && sumb <= kSmallMaxSumb && P.use_small && (sumb > 0 || P.small0)) {
+        // K2s (gpzb_encode_small.cuh): with offsets from the front of the list, offset-free from the back
+        rec.kind = KIND_SMALL;
+        if (sumb) P.small_list[atomicAdd(&R->small_count, 1u)] = (uint32_t)blk;
+        else P.small_list[P.nblocks - 1 - atomicAdd(&R->small0_count, 1u)] = (uint32_t)blk;
+      } else if (sumb == 0 && PN <= kWarpEncMaxPN && full) {
         rec.kind = KIND_WARP;
         atomicAdd(&R->warp_count, 1u);
       } else {
         rec.kind = KIND_NARROW;
-        if (P.cta_list) P.cta_list[atomicAdd(&R->cta_count, 1u)] = (uint32_t)blk;
+        P.cta_list[atomicAdd(&R->cta_count, 1u)] = (uint32_t)blk;
       }
     } else {
       rec.kind = KIND_WIDE;

@@ -451,11 +451,11 @@ __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncPara
   __shared__ NarrowSmem sm;
   const int tid = threadIdx.x;
   using T = typename std::conditional<F64, double, float>::type;
-  // one block per CTA: block i in launch order when every narrow block is
-  // ours, else entry i of K1.5's list (the grid is sized to it)
-  {
-    if (P.cta_mode == 2 && blockIdx.x >= *reinterpret_cast<volatile const uint32_t*>(&P.res->cta_count)) return;
-    const uint64_t blk = P.cta_mode ? (uint64_t)P.cta_list[blockIdx.x] : (uint64_t)blockIdx.x;
+  // persistent over K1.5's list of narrow blocks (plus the blocks K2s handed
+  // back); the list length is read on the device, so the host never waits
+  const uint32_t count = *reinterpret_cast<volatile const uint32_t*>(&P.res->cta_count);
+  for (uint32_t item = blockIdx.x; item < count; item += gridDim.x) {
+    const uint64_t blk = (uint64_t)P.cta_list[item];
     const uint64_t first = blk * (uint64_t)P.bs;
     const int n = (int)min((uint64_t)P.bs, P.count - first);
     const bool full = n == kMaxBs && P.vec;
@@ -464,9 +464,11 @@ __global__ void __launch_bounds__(kThreads, GPZB_K2_MINB) k_encode(const EncPara
     if (tid < 8) reinterpret_cast<uint4*>(&sm.rec)[tid] = reinterpret_cast<const uint4*>(P.rec + blk)[tid];
     __syncthreads();
     const BlkRec* rec = &sm.rec;
-    if (rec->kind != KIND_NARROW) return;  // cta_mode 0: general / error blocks are sized elsewhere
-    if (full) narrow_body<D, F64, true>(P, sm, blk, rec, n, x);
-    else narrow_body<D, F64, false>(P, sm, blk, rec, n, x);
+    if (rec->kind == KIND_NARROW) {  // block-uniform
+      if (full) narrow_body<D, F64, true>(P, sm, blk, rec, n, x);
+      else narrow_body<D, F64, false>(P, sm, blk, rec, n, x);
+    }
+    __syncthreads();  // the shared state is reused by the next block
   }
 }
 

@@ -1,0 +1,469 @@
+// K2s: persistent CTA encoder for full float32 blocks with at most four
+// offset bits per particle (Σ log2 m <= 4, Π N <= 2^16) — the bulk of
+// HACC-like snapshots at rel-eb 1e-3 (velocities: log2 m = 1 or 2 per axis;
+// positions: log2 m = 0).  Same bytes as pipeline._encode_block
+// (pipeline.py:38-70).  One CTA of 128 threads per block, 8 particles and 8
+// runs per thread, CTAs persistent over K1.5's block list.
+//
+// Per block (9 barriers with offsets, 7 without):
+//   quantize (certified reciprocal, quantizer.py:142-191) -> 32-bit key
+//        seg | off << 16 per particle; RED.OR into a presence bitmap over
+//        [0, Π N)                                                     | B1
+//   word prefixes of the bitmap (up to four 16-byte groups per thread) | B2 B3
+//   segment rank r of each particle = prefix + popc below its bit; the
+//        rank's counter word gets 1 << 4*off (ATOMS: the returned nibble is
+//        the particle's tie index among identical (seg, off) pairs); the
+//        unique id of rank r goes to uniq[r + 1]                      | B4
+//        == rle_encode(sort_block(...)) (codec.py:53-79, blocksort.py:17-28)
+//   thread t owns runs 8t..8t+7: count = nibble sum of the counter word,
+//        delta = uniq[r + 1] - uniq[r] (delta_encode, codec.py:93-100);
+//        one scan of the counts (run starts) + OR of the widths
+//        (width_for, codec.py:107-112)                                | B5
+//   header + delta + count streams bit-packed into the shared stage
+//        (serialize_block / pack_fixed, container.py:102-121,
+//        codec.py:115-129)                                            | B6
+//   each particle's place in (seg, off) order = run start + particles of
+//        its run with a smaller offset (nibble sum below its nibble) + tie;
+//        its offset goes there                                        | B7
+//   the offset stream packed from the ordered offsets; bitmap and counters
+//        zeroed for the next block                                    | B8
+//   the stage to the block's staging slot (K3 concatenates), stage zeroed
+//        (it is the next block's bitmap)                              | B9
+//
+// A (segment, offset) pair held by >= 16 particles overflows its nibble (or,
+// for Σ log2 m <= 3, a run of >= 16 particles defeats the one-multiply
+// nibble sum); either way the counts then sum to less than 1024 and the
+// block is handed to the general CTA encoder K2 (gpzb_encode_narrow.cuh)
+// through its list — exact in every case.
+#pragma once
+
+#include "gpzb_encode_narrow.cuh"
+
+namespace gpzb {
+
+#ifndef GPZB_K2S_MINB
+#define GPZB_K2S_MINB 6
+#endif
+#ifndef GPZB_K2S0_MINB
+#define GPZB_K2S0_MINB 7
+#endif
+constexpr int kST = 128;               // K2s threads per block
+constexpr int kSW = kST / 32;          // warps per block
+constexpr int kSP = kMaxBs / kST;      // particles (and runs) per thread
+constexpr uint32_t kSmallMaxPN = 65536;
+// payload <= 50 + 1024 * 16 / 8 + 1024 * 11 / 8 (no offsets) = 3,506 bytes
+// (with offsets: counts <= 8 bits, offsets <= 4 bits: 3,634 bytes)
+constexpr int kSmallStageWords = 1024;
+
+template <int D, bool HAS_OFF>
+struct SmallSmem {
+  // this block's coordinates and geometry record, brought in by one bulk
+  // copy (TMA, cp.async.bulk) issued while the previous block was encoded
+  __align__(128) float x[D][kMaxBs];
+  __align__(16) BlkRec rec;
+  unsigned long long mbar;               // completion barrier of that copy
+  uint32_t blk;                          // the block it holds
+  __align__(16) uint32_t scan[2][kSW];   // warp totals of the two block scans
+  __align__(16) uint32_t orw[4];         // width ORs: counts, deltas, offsets
+  // presence bitmap over segments (quantize .. ranks), then the payload stage
+  __align__(16) uint32_t bm[kSmallMaxPN / 32];
+  union {
+    uint16_t wp[kSmallMaxPN / 32];       // set bits before each bitmap word (prefix .. ranks)
+    struct {
+      uint16_t rstart[kMaxBs];           // first sorted position of run r
+      uint8_t soff[kMaxBs];              // offsets in (seg, off) order
+    } o;
+  } u;
+  // per segment rank: two words of 8 nibble counters by offset (or the count)
+  __align__(16) uint32_t cnt[HAS_OFF ? 2 * kMaxBs : kMaxBs];
+  __align__(16) uint16_t uniq[kMaxBs + 8];  // [0] = 0 sentinel, [r + 1] = unique id of rank r
+};
+static_assert(kSmallStageWords <= kSmallMaxPN / 32, "the stage reuses the bitmap");
+
+// Exclusive scan of one value per thread over the (kSW-warp) CTA with a
+// single barrier.  `ws` (16-byte aligned) is not rewritten before a later
+// barrier.
+__device__ __forceinline__ uint32_t small_excl_scan(uint32_t v, uint32_t& total, uint32_t* ws) {
+  static_assert(kSW == 4, "one 16-byte read of the warp totals");
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[wid] = x;
+  __syncthreads();
+  const uint4 a = *reinterpret_cast<const uint4*>(ws);
+  const uint32_t b1 = a.x, b2 = b1 + a.y, b3 = b2 + a.z;
+  total = b3 + a.w;
+  const uint32_t before = wid == 0 ? 0u : (wid == 1 ? b1 : (wid == 2 ? b2 : b3));
+  return before + x - v;
+}
+
+// Sum of the nibbles of a counter word (each nibble <= 15).  Exact when the
+// sum is <= 15 (one multiply), the case of runs of <= 15 particles, which
+// Σ log2 m <= 3 blocks must have (a longer run reads short, and the
+// block-level count check hands the block back).
+__device__ __forceinline__ uint32_t nib_sum1(uint32_t x) { return (x * 0x11111111u) >> 28; }
+// Exact for any word (byte-wise fold first).
+__device__ __forceinline__ uint32_t nib_sum8(uint32_t x) {
+  const uint32_t s = (x & 0x0f0f0f0fu) + ((x >> 4) & 0x0f0f0f0fu);  // bytes <= 30
+  return (s * 0x01010101u) >> 24;
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// One bulk copy of block `blk`'s coordinates and geometry record into shared
+// memory, completing on the CTA's mbarrier (one elected thread).
+template <int D>
+__device__ __forceinline__ void small_fetch(const EncParams& P, SmallSmem<D, true>* s0, SmallSmem<D, false>* s1,
+                                            uint32_t blk) {
+  float(*x)[kMaxBs] = s0 ? s0->x : s1->x;
+  BlkRec* r = s0 ? &s0->rec : &s1->rec;
+  unsigned long long* bar = s0 ? &s0->mbar : &s1->mbar;
+  mbar_expect_tx(reinterpret_cast<uint64_t*>(bar), D * kMaxBs * 4 + (uint32_t)sizeof(BlkRec));
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+    bulk_g2s(x[a], reinterpret_cast<const float*>(P.axes[a]) + (uint64_t)blk * kMaxBs, kMaxBs * 4,
+             reinterpret_cast<uint64_t*>(bar));
+  bulk_g2s(r, P.rec + blk, sizeof(BlkRec), reinterpret_cast<uint64_t*>(bar));
+}
+
+template <int D, bool HAS_OFF>
+__global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB) k_encode_small(const EncParams P) {
+  static_assert(kSP == 8, "thread t owns runs 8t..8t+7");
+  using Smem = SmallSmem<D, HAS_OFF>;
+  __shared__ Smem sm;
+  constexpr uint32_t H = 8 + D * 13 + 3;  // F32 block header bytes (container.py:62-67)
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  DevResult* R = P.res;
+  const uint32_t nlist = HAS_OFF ? *reinterpret_cast<volatile const uint32_t*>(&R->small_count)
+                                 : *reinterpret_cast<volatile const uint32_t*>(&R->small0_count);
+  if (blockIdx.x >= nlist) return;
+  auto list_at = [&](uint32_t i) -> uint32_t {
+    return HAS_OFF ? P.small_list[i] : P.small_list[P.nblocks - 1 - i];
+  };
+  auto fetch = [&](uint32_t blk) {
+    if constexpr (HAS_OFF) small_fetch<D>(P, &sm, nullptr, blk);
+    else small_fetch<D>(P, nullptr, &sm, blk);
+  };
+  const uint4 z4 = make_uint4(0, 0, 0, 0);
+  // invariant at every block start: bitmap (= stage), counters and OR words are zero
+  for (int i = tid; i < (int)(kSmallMaxPN / 128); i += kST) reinterpret_cast<uint4*>(sm.bm)[i] = z4;
+  for (int i = tid; i < (int)(sizeof(sm.cnt) / 16); i += kST) reinterpret_cast<uint4*>(sm.cnt)[i] = z4;
+  if (tid < 4) sm.orw[tid] = 0;
+  if (tid == 0) {
+    sm.uniq[0] = 0;
+    mbar_init(reinterpret_cast<uint64_t*>(&sm.mbar), 1);
+    mbar_fence_init();
+    sm.blk = list_at(blockIdx.x);
+    fetch(sm.blk);
+  }
+  __syncthreads();
+
+  const uint32_t bm_s = smem_u32(sm.bm);
+  uint32_t phase = 0;
+  for (uint32_t item = blockIdx.x; item < nlist; item += gridDim.x) {
+    mbar_wait(reinterpret_cast<uint64_t*>(&sm.mbar), phase);
+    phase ^= 1;
+    const uint64_t blk = sm.blk;
+    const BlkRec& rec = sm.rec;
+    // thread t: particles 4t..4t+3 and 512+4t..512+4t+3 of sm.x
+    auto xat = [&](int a, int k) -> float { return sm.x[a][(k < 4 ? 4 * tid : 4 * (kST + tid)) + (k & 3)]; };
+    const uint32_t PN = rec.PN;
+    const uint32_t sumb = HAS_OFF ? (uint32_t)rec.sumb : 0u;
+
+    // ---- quantize -> key = seg | off << 16; presence bitmap over segments
+    uint32_t key[kSP], off_or = 0;
+    {
+      uint32_t seg[kSP], off[kSP];
+#pragma unroll
+      for (int k = 0; k < kSP; ++k) { seg[k] = 0; off[k] = 0; }
+      uint32_t lowmin = ~0u;  // min over coordinates of (low word of r) + 1: <= 1 flags a possible failure
+      uint32_t stride = 1, shift = 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const double lo = rec.lo[a], rinv = rec.rinv[a];
+        const uint32_t b = HAS_OFF ? (uint32_t)rec.b[a] : 0u;
+        const uint32_t mks = ((1u << b) - 1u) << shift;
+        float x[kSP];
+        {
+          const float4 v0 = reinterpret_cast<const float4*>(sm.x[a])[tid];
+          const float4 v1 = reinterpret_cast<const float4*>(sm.x[a])[kST + tid];
+          x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
+          x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
+        }
+#pragma unroll
+        for (int k = 0; k < kSP; ++k) {
+          // certified reciprocal quantizer (gpzb_common.cuh quantize_coord,
+          // mode 0); r == 0 (t == 0) is exact, its high word is zero
+          const double t = __dsub_rn((double)x[k], lo);
+          const double r = __dmul_rn(t, rinv);
+          const uint32_t rl = (uint32_t)__double2loint(r);
+          const uint32_t q = (uint32_t)__double2loint(__dadd_rz(r, 4503599627370496.0));
+          lowmin = min(lowmin, rl + 1u);
+          if (HAS_OFF) {
+            seg[k] += (q >> b) * stride;
+            off[k] |= (q << shift) & mks;
+          } else {
+            seg[k] += q * stride;
+          }
+        }
+        stride *= rec.N[a];
+        shift += b;
+      }
+      // rare: some low word is 0 or all ones.  Exact zeros (t == 0, the
+      // block minimum) pass the certificate; anything else is redone by
+      // exact division (identical wherever the certificate holds)
+      bool bad = false;
+      if (__any_sync(kFull, lowmin <= 1u) && lowmin <= 1u) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const double lo = rec.lo[a], rinv = rec.rinv[a];
+#pragma unroll
+          for (int k = 0; k < kSP; ++k) {
+            const double r = __dmul_rn(__dsub_rn((double)xat(a, k), lo), rinv);
+            const uint32_t rl = (uint32_t)__double2loint(r), rh = (uint32_t)__double2hiint(r);
+            bad |= ((rl + 1u) <= 1u) & (rh != 0u);
+          }
+        }
+      }
+      if (__any_sync(kFull, bad) && bad) {
+#pragma unroll
+        for (int k = 0; k < kSP; ++k) {
+          const uint64_t so = redo_exact<D, float>(xat(0, k), D > 1 ? xat(D > 1 ? 1 : 0, k) : 0.f,
+                                                   D > 2 ? xat(D > 2 ? 2 : 0, k) : 0.f, &rec);
+          seg[k] = (uint32_t)(so >> 32);
+          off[k] = (uint32_t)so;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kSP; ++k) {
+        key[k] = seg[k] | (off[k] << 16);
+        off_or |= off[k];
+        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(bm_s + ((seg[k] >> 3) & ~3u)), "r"(1u << (seg[k] & 31))
+                     : "memory");
+      }
+    }
+    const uint32_t w_hdr_b = HAS_OFF && lane < D ? (uint32_t)rec.b[lane] : 0u;  // header fields, read before
+    const uint32_t w_hdr_n = lane < D ? rec.N[lane] : 0u;                       // the record is overwritten
+    __syncthreads();  // B1: coordinates and record consumed
+    if (tid == 0 && item + gridDim.x < nlist) {  // the next block's bulk copy overlaps this block's encode
+      fence_proxy_async_smem();
+      sm.blk = list_at(item + gridDim.x);
+      fetch(sm.blk);
+    }
+
+    // ---- bitmap word prefixes: thread t owns 16-byte groups [t*gpt, t*gpt + gpt)
+    const uint32_t ng = (((PN + 31) >> 5) + 3) >> 2;  // <= 512
+    const uint32_t gpt = (ng + kST - 1) / kST;         // <= 4, block-uniform
+    uint32_t U;
+    {
+      uint32_t l = 0;
+      for (uint32_t i = 0; i < gpt; ++i) {
+        const uint32_t g = tid * gpt + i;
+        if (g < ng) {
+          const uint4 q = reinterpret_cast<const uint4*>(sm.bm)[g];
+          l += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+        }
+      }
+      uint32_t e = small_excl_scan(l, U, sm.scan[0]);  // B2
+      for (uint32_t i = 0; i < gpt; ++i) {
+        const uint32_t g = tid * gpt + i;
+        if (g < ng) {
+          const uint4 q = reinterpret_cast<const uint4*>(sm.bm)[g];
+          const uint32_t e1 = e + __popc(q.x), e2 = e1 + __popc(q.y), e3 = e2 + __popc(q.z);
+          reinterpret_cast<uint2*>(sm.u.wp)[g] = make_uint2(e | (e1 << 16), e2 | (e3 << 16));
+          e = e3 + __popc(q.w);
+        }
+      }
+    }
+    __syncthreads();  // B3
+
+    // ---- segment ranks -> counters (tie index returned), unique ids
+    uint32_t rk[kSP];
+#pragma unroll
+    for (int k = 0; k < kSP; ++k) {
+      const uint32_t sg = key[k] & 0xffffu, w = sg >> 5;
+      const uint32_t r = (uint32_t)sm.u.wp[w] + __popc(sm.bm[w] & ((1u << (sg & 31)) - 1u));
+      sm.uniq[r + 1] = (uint16_t)sg;
+      if (HAS_OFF) {
+        const uint32_t o = key[k] >> 16, sh = 4 * (o & 7);
+        const uint32_t old = atomicAdd(&sm.cnt[2 * r + (o >> 3)], 1u << sh);
+        rk[k] = r | ((old >> sh) & 15u) << 10 | o << 14;
+      } else {
+        atomicAdd(&sm.cnt[r], 1u);  // result unused: RED
+        rk[k] = r;
+      }
+    }
+    __syncthreads();  // B4: bitmap and word prefixes dead
+
+    // ---- runs 8t..8t+7: counts, deltas; run starts (scan) and stream widths (OR)
+    const bool wide = sumb > 3;  // counters in both words of a rank
+    uint32_t dc[kSP], csum = 0, c_or = 0, d_or = 0;
+    {
+      const uint4 u4 = reinterpret_cast<const uint4*>(sm.uniq)[tid];
+      const uint32_t u[9] = {u4.x & 0xffffu, u4.x >> 16, u4.y & 0xffffu, u4.y >> 16,
+                             u4.z & 0xffffu, u4.z >> 16, u4.w & 0xffffu, u4.w >> 16, (uint32_t)sm.uniq[kSP * tid + kSP]};
+      uint32_t cc[kSP];
+      if (HAS_OFF) {
+#pragma unroll
+        for (int j = 0; j < kSP; j += 2) {
+          const uint4 c2 = reinterpret_cast<const uint4*>(sm.cnt)[(kSP * tid + j) >> 1];
+          cc[j] = wide ? nib_sum8(c2.x) + nib_sum8(c2.y) : nib_sum1(c2.x);
+          cc[j + 1] = wide ? nib_sum8(c2.z) + nib_sum8(c2.w) : nib_sum1(c2.z);
+        }
+      } else {
+        const uint4 c0 = reinterpret_cast<const uint4*>(sm.cnt)[2 * tid], c1 = reinterpret_cast<const uint4*>(sm.cnt)[2 * tid + 1];
+        cc[0] = c0.x; cc[1] = c0.y; cc[2] = c0.z; cc[3] = c0.w; cc[4] = c1.x; cc[5] = c1.y; cc[6] = c1.z; cc[7] = c1.w;
+      }
+#pragma unroll
+      for (int j = 0; j < kSP; ++j) {
+        const bool in = (uint32_t)(kSP * tid + j) < U;
+        const uint32_t c = in ? cc[j] : 0u;
+        const uint32_t d = in ? u[j + 1] - u[j] : 0u;
+        csum += c;
+        c_or |= c;
+        d_or |= d;
+        dc[j] = d | (c << 16);
+      }
+    }
+    // the bitmap becomes the payload stage: zero the words it used
+    for (uint32_t g = tid; g < ng; g += kST) reinterpret_cast<uint4*>(sm.bm)[g] = z4;
+    if (!HAS_OFF && kSP * tid < (int)U) {  // counters are dead too (offset-free blocks)
+      reinterpret_cast<uint4*>(sm.cnt)[2 * tid] = z4;
+      reinterpret_cast<uint4*>(sm.cnt)[2 * tid + 1] = z4;
+    }
+    uint32_t total, ex;
+    {
+      const uint32_t r0 = __reduce_or_sync(kFull, c_or), r1 = __reduce_or_sync(kFull, d_or);
+      const uint32_t r2 = HAS_OFF ? __reduce_or_sync(kFull, off_or) : 0u;
+      const uint32_t mine = lane == 0 ? r0 : (lane == 1 ? r1 : r2);
+      red_or_shared_if(lane < 3 && mine != 0, &sm.orw[lane < 3 ? lane : 0], mine);
+      ex = small_excl_scan(csum, total, sm.scan[1]);  // B5
+    }
+    if (HAS_OFF && total != (uint32_t)kMaxBs) {
+      // a nibble counter overflowed: the general CTA encoder takes this block
+      // (block-uniform branch; nothing was written to the stage)
+      if (kSP * tid < (int)U) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) reinterpret_cast<uint4*>(sm.cnt)[4 * tid + i] = z4;
+      }
+      if (tid < 4) sm.orw[tid] = 0;
+      if (tid == 0) {
+        P.rec[blk].kind = KIND_NARROW;
+        P.cta_list[atomicAdd(&R->cta_count, 1u)] = (uint32_t)blk;
+      }
+      __syncthreads();
+      continue;
+    }
+    const uint32_t w_cnt = bitlen32(sm.orw[0]), w_del = bitlen32(sm.orw[1]);
+    const uint32_t w_off = HAS_OFF ? bitlen32(sm.orw[2]) : 0u;
+    const uint32_t Ld = (U * w_del + 7) >> 3, Lc = (U * w_cnt + 7) >> 3;
+    const uint32_t Lo = HAS_OFF ? ((uint32_t)kMaxBs * w_off + 7) >> 3 : 0u;
+    const uint32_t L = H + Ld + Lc + Lo;
+    const uint32_t bd = 8 * H, bc = bd + 8 * Ld, bo = bc + 8 * Lc;
+    if (tid == 0) {
+      P.status[blk] = L;  // payload length for the K3 scan
+      P.rec[blk].path = HAS_OFF ? 6 : 7;  // diagnostics: gpzb_encode_path_counts
+    }
+    if (HAS_OFF && kSP * tid < (int)U) {  // run starts of runs 8t..8t+7 (one 16-byte store)
+      uint32_t e[kSP];
+      e[0] = ex;
+#pragma unroll
+      for (int j = 1; j < kSP; ++j) e[j] = e[j - 1] + (dc[j - 1] >> 16);
+      reinterpret_cast<uint4*>(sm.u.o.rstart)[tid] =
+          make_uint4(e[0] | e[1] << 16, e[2] | e[3] << 16, e[4] | e[5] << 16, e[6] | e[7] << 16);
+    }
+    uint32_t* st = sm.bm;  // the payload stage
+    // block header, one field per lane of warp 0 (container.serialize_block, container.py:107-121)
+    if (wid == 0) {
+      const int f = lane;
+      uint32_t bpos = 0, val = 0;
+      const int a = (f - 2) >> 2, which = (f - 2) & 3;
+      const uint32_t hb = __shfl_sync(kFull, w_hdr_b, a & 3), hn = __shfl_sync(kFull, w_hdr_n, a & 3);
+      if (f == 0) { bpos = 0; val = (uint32_t)kMaxBs; }
+      else if (f == 1) { bpos = 4; val = U; }
+      else if (f < 2 + 4 * D) {
+        const uint32_t ab = 8 + a * 13;
+        if (which < 2) {
+          bpos = ab + which * 4;
+          val = __float_as_uint(reinterpret_cast<const float*>(P.bounds)[blk * 2 * D + 2 * a + which]);
+        } else if (which == 2) { bpos = ab + 8; val = hb; }
+        else { bpos = ab + 9; val = hn; }
+      } else if (f < 2 + 4 * D + 3) {
+        const int wi = f - 2 - 4 * D;
+        bpos = 8 + D * 13 + wi;
+        val = wi == 0 ? w_del : (wi == 1 ? w_cnt : w_off);
+      }
+      if (f < 2 + 4 * D + 3) or_bits(st, 8ull * bpos, val);
+    }
+    // deltas + run lengths of runs 8t..8t+7, four values per 64-bit window
+    if (kSP * tid < (int)U) {
+      const uint32_t r0 = kSP * tid;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t* v = dc + 4 * h;
+        if (w_del)
+          or_bits(st, bd + (r0 + 4 * h) * w_del,
+                  (uint64_t)(v[0] & 0xffffu) | (uint64_t)(v[1] & 0xffffu) << w_del |
+                      (uint64_t)(v[2] & 0xffffu) << (2 * w_del) | (uint64_t)(v[3] & 0xffffu) << (3 * w_del));
+        or_bits(st, bc + (r0 + 4 * h) * w_cnt,
+                (uint64_t)(v[0] >> 16) | (uint64_t)(v[1] >> 16) << w_cnt | (uint64_t)(v[2] >> 16) << (2 * w_cnt) |
+                    (uint64_t)(v[3] >> 16) << (3 * w_cnt));
+      }
+    }
+    if (HAS_OFF) {
+      __syncthreads();  // B6: run starts visible
+      // ---- offsets into (seg, off) order
+#pragma unroll
+      for (int k = 0; k < kSP; ++k) {
+        const uint32_t r = rk[k] & 0x3ffu, o = rk[k] >> 14;
+        const uint32_t m = (1u << (4 * (o & 7))) - 1u;
+        uint32_t below;
+        if (wide) {
+          const uint2 c = reinterpret_cast<const uint2*>(sm.cnt)[r];
+          below = o < 8 ? nib_sum8(c.x & m) : nib_sum8(c.x) + nib_sum8(c.y & m);
+        } else {
+          below = nib_sum1(sm.cnt[2 * r] & m);
+        }
+        sm.u.o.soff[(uint32_t)sm.u.o.rstart[r] + below + ((rk[k] >> 10) & 15u)] = (uint8_t)o;
+      }
+      __syncthreads();  // B7
+      if (w_off) {  // sorted offsets 8t..8t+7 (each < 16): one 32-bit window
+        const uint2 o8 = reinterpret_cast<const uint2*>(sm.u.o.soff)[tid];
+        uint32_t v = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          v |= ((o8.x >> (8 * j)) & 0xffu) << (j * w_off);
+          v |= ((o8.y >> (8 * j)) & 0xffu) << ((j + 4) * w_off);
+        }
+        or_bits32(st, bo + kSP * tid * w_off, v);
+      }
+      // counters and OR words are dead: zero them for the next block
+      if (kSP * tid < (int)U) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) reinterpret_cast<uint4*>(sm.cnt)[4 * tid + i] = z4;
+      }
+      if (tid < 4) sm.orw[tid] = 0;
+    }
+    __syncthreads();  // B8: the stage is complete
+    if (!HAS_OFF && tid < 4) sm.orw[tid] = 0;
+    // ---- the stage to this block's 16-byte aligned staging slot (K3 moves it
+    // into place); the stage words are zeroed behind the copy (bitmap invariant)
+    {
+      uint4* slot = reinterpret_cast<uint4*>(P.staging + blk * (uint64_t)kSlotBytes);
+      const uint32_t nq = (L + 15) >> 4;
+      for (uint32_t w = tid; w < nq; w += kST) {
+        __stcg(slot + w, reinterpret_cast<const uint4*>(st)[w]);
+        reinterpret_cast<uint4*>(st)[w] = z4;
+      }
+    }
+    __syncthreads();  // B9: the zeroed stage is the next block's bitmap
+  }
+}
+
+}  // namespace gpzb

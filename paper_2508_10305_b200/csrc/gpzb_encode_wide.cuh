@@ -350,6 +350,12 @@ __global__ void __launch_bounds__(kThreads) k_encode_wide(const EncParams P) {
   if (err) continue;  // cannot happen: K1.5 routes error blocks elsewhere
 
   // ---- 9. bit-pack header + streams into the realigned stage
+  if (rec->side_off + ((L + 15) & ~15ull) > P.side_cap) {
+    // the caller's side buffer is too small: report the bytes K1.5 reserved
+    // (the host grows the buffer and encodes again); nothing is written
+    if (tid == 0) atomicMax(&R->side_need, R->side_bytes);
+    continue;
+  }
   uint8_t* dst = P.side + rec->side_off;  // 16B aligned
   const uint32_t al = 0;
   const uint32_t nbytes = al + (uint32_t)L;

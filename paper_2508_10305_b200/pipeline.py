@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import struct
+import threading
 from typing import Iterator
 
 import numpy as np
@@ -51,18 +52,45 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
-_WS: dict = {}
+# Every scratch buffer and helper stream is cached per *thread* (and device
+# and slot): calls from different threads never share a workspace, a side
+# buffer, a pinned staging buffer or a stream, so concurrent compress /
+# decompress calls on distinct data are safe, as the reference's pure
+# functions are.
+_TLS = threading.local()
+
+
+def _tls(name: str) -> dict:
+    d = getattr(_TLS, name, None)
+    if d is None:
+        d = {}
+        setattr(_TLS, name, d)
+    return d
 
 
 def _workspace(nbytes: int, slot: int = 0) -> torch.Tensor:
-    """Per-device scratch, grown on demand (the library never allocates);
-    one buffer per concurrent slot (compress_batch_device)."""
+    """Per-thread, per-device scratch, grown on demand (the library never
+    allocates); one buffer per concurrent slot (compress_batch_device)."""
     dev = _device()
+    cache = _tls("ws")
     key = (dev.index, slot)
-    buf = _WS.get(key)
+    buf = cache.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=dev)
-        _WS[key] = buf
+        cache[key] = buf
+    return buf
+
+
+def _side(slot: int, nbytes: int = 0) -> torch.Tensor:
+    """Side buffer for the general encoder's payloads (K2w), cached like the
+    workspace; it only grows when a compression reports GPZB_NEED_SIDE."""
+    dev = _device()
+    cache = _tls("side")
+    key = (dev.index, slot)
+    buf = cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+        cache[key] = buf
     return buf
 
 
@@ -119,7 +147,7 @@ class _Job:
     """One dataset's compression in flight (the phases of compress_device)."""
 
     __slots__ = ("axes", "ptrs", "count", "dims", "prec", "bs", "t", "pres", "eb", "mode", "ws", "out", "bound",
-                 "nb", "res", "stream", "timing")
+                 "nb", "res", "stream", "timing", "slot", "words")
 
 
 def _ev():
@@ -138,6 +166,7 @@ def _compress_begin(ds, cfg: CompressConfig, slot: int, timing, plan: bool = Tru
     j.bs, j.t, j.pres = cfg.block_size, cfg.target_segs_per_axis, int(cfg.preserve_order)
     j.eb, j.mode = float(cfg.error_bound), cfg.eb_mode.value
     j.timing = timing
+    j.slot, j.words = slot, None
     ws_bytes = ctypes.c_uint64()
     _check(lib.gpzb_compress_workspace(j.count, j.dims, j.prec, j.bs, ctypes.byref(ws_bytes)))
     bound = ctypes.c_uint64()
@@ -169,27 +198,42 @@ def _compress_plan(j: _Job) -> None:
 
 
 def _compress_encode(j: _Job) -> None:
-    """Read K1.5's routing (one sync of the job's stream) and enqueue K2 + K3."""
+    """Enqueue the encoders + K3 (no host sync: every encoder reads its block
+    count on the device)."""
     if j.count == 0:
         return
-    side_bytes, cta_b, warp_b = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
-    _check(lib.gpzb_encode_plan_counts(j.ws.data_ptr(), j.ws.numel(), j.stream, ctypes.byref(side_bytes),
-                                        ctypes.byref(cta_b), ctypes.byref(warp_b)))
-    side = torch.empty(max(side_bytes.value, 16), dtype=torch.uint8, device=j.axes[0].device)
+    side = _side(j.slot)
     e0 = _ev() if j.timing is not None else None
     _check(lib.gpzb_encode_async(j.ptrs, j.dims, j.prec, j.count, j.eb, j.mode, j.bs, j.t, j.pres, j.ws.data_ptr(),
-                                 j.ws.numel(), side.data_ptr(), side_bytes.value, j.out.data_ptr(), j.bound, 0,
-                                 j.count, j.nb, 1, cta_b.value, warp_b.value, j.stream))
+                                 j.ws.numel(), side.data_ptr(), side.numel(), j.out.data_ptr(), j.bound, 0,
+                                 j.count, j.nb, 1, j.stream))
     if j.timing is not None:
         j.timing.setdefault("encode", []).append((e0, _ev()))
 
 
 def _compress_status(j: _Job) -> int:
-    """Read the result record (one sync of the job's stream); no raising."""
+    """Read the result record (one sync of the job's stream); no raising.
+    When general-encoder blocks outgrew the cached side buffer the library
+    wrote nothing for them and reports the size: grow it and encode again
+    (the range words of a sharded run are restored from j.words)."""
     if j.count == 0:
         return lib.gpzb_compress(j.ptrs, j.dims, j.prec, j.count, j.eb, j.mode, j.bs, j.t, j.pres, j.ws.data_ptr(),
                                  j.ws.numel(), j.out.data_ptr(), j.bound, j.stream, ctypes.byref(j.res))
-    return lib.gpzb_compress_result(j.ws.data_ptr(), j.ws.numel(), j.count, j.bs, j.stream, ctypes.byref(j.res))
+    st = lib.gpzb_compress_result(j.ws.data_ptr(), j.ws.numel(), j.count, j.bs, j.stream, ctypes.byref(j.res))
+    if st == _lib.NEED_SIDE:
+        _side(j.slot, j.res.side_bytes)
+        with torch.cuda.stream(torch.cuda.ExternalStream(j.stream)):
+            _check(lib.gpzb_workspace_reset_async(j.ws.data_ptr(), j.ws.numel(), j.count, j.bs, j.stream))
+            _check(lib.gpzb_range_async(j.ptrs, j.dims, j.prec, j.count, j.bs, j.ws.data_ptr(), j.ws.numel(),
+                                        j.stream))
+            if j.words is not None:
+                j.ws[40:56].view(torch.int64).copy_(j.words)
+            _compress_plan(j)
+            timing, j.timing = j.timing, None
+            _compress_encode(j)
+            j.timing = timing
+        st = lib.gpzb_compress_result(j.ws.data_ptr(), j.ws.numel(), j.count, j.bs, j.stream, ctypes.byref(j.res))
+    return st
 
 
 def _compress_finish(j: _Job) -> torch.Tensor:
@@ -197,18 +241,15 @@ def _compress_finish(j: _Job) -> torch.Tensor:
     st = _compress_status(j)
     _check(st, j.res)
     compress_device.last_result = j.res
-    _LAST.update(ws=j.ws, count=j.count, bs=j.bs, dims=j.dims, prec=j.prec)
+    _tls("last").update(ws=j.ws, count=j.count, bs=j.bs, dims=j.dims, prec=j.prec)
     return j.out[: j.res.out_len]
 
 
-_LAST: dict = {}
-
-
 def last_path_counts() -> list:
-    """Diagnostics: blocks per offset-order path of the last compression
+    """Diagnostics: blocks per encoder path of this thread's last compression
     (include/gpzb.h gpzb_encode_path_counts)."""
-    c = (ctypes.c_uint64 * 6)()
-    w = _LAST
+    c = (ctypes.c_uint64 * 8)()
+    w = _tls("last")
     _check(lib.gpzb_encode_path_counts(w["ws"].data_ptr(), w["ws"].numel(), w["count"], w["bs"], w["dims"],
                                        w["prec"], _stream(), c))
     return list(c)
@@ -226,19 +267,18 @@ def compress_device(ds, cfg: CompressConfig, *, timing=None) -> torch.Tensor:
     return _compress_finish(j)
 
 
-_STREAMS: dict = {}
-
-
 def _side_stream(i: int) -> torch.cuda.Stream:
-    """Stream i of the batched calls: earlier datasets get higher priority, so
-    the first range pass finishes first and its encoder starts while the next
-    range pass still streams (a pipeline instead of two halves contending)."""
+    """Stream i of the batched calls (per thread): earlier datasets get higher
+    priority, so the first range pass finishes first and its encoder starts
+    while the next range pass still streams (a pipeline instead of two halves
+    contending)."""
     dev = _device()
+    streams = _tls("streams")
     key = (dev.index, i)
-    if key not in _STREAMS:
+    if key not in streams:
         lo, hi = torch.cuda.Stream.priority_range()  # (lowest, highest); higher priority = smaller number
-        _STREAMS[key] = torch.cuda.Stream(device=dev, priority=max(hi, min(lo, hi + i)))
-    return _STREAMS[key]
+        streams[key] = torch.cuda.Stream(device=dev, priority=max(hi, min(lo, hi + i)))
+    return streams[key]
 
 
 def compress_batch_device(datasets, cfg: CompressConfig, *, timing=None) -> list:
@@ -268,14 +308,13 @@ def compress_batch_device(datasets, cfg: CompressConfig, *, timing=None) -> list
     return outs
 
 
-_PINNED: dict = {}
-
-
 def _pinned(nbytes: int) -> torch.Tensor:
-    buf = _PINNED.get("out")
+    """This thread's pinned host staging buffer (grown on demand)."""
+    cache = _tls("pinned")
+    buf = cache.get("out")
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
-        _PINNED["out"] = buf
+        cache["out"] = buf
     return buf
 
 
@@ -463,14 +502,12 @@ def decompress_batch_device(containers, *, timing=None) -> list:
     return out
 
 
-_COPY_STREAM: dict = {}
-
-
 def _copy_stream(i: int = 0) -> torch.cuda.Stream:
     dev = _device()
-    st = _COPY_STREAM.get((dev.index, i))
+    streams = _tls("copy_streams")
+    st = streams.get((dev.index, i))
     if st is None:
-        st = _COPY_STREAM[(dev.index, i)] = torch.cuda.Stream(device=dev)
+        st = streams[(dev.index, i)] = torch.cuda.Stream(device=dev)
     return st
 
 

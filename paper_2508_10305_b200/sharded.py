@@ -107,6 +107,8 @@ class _CudaHooks:
         return self.ws[40:56].view(torch.int64)  # DevResult.range_w, in place
 
     def local_encode(self, global_count: int, global_blocks: int):
+        from .pipeline import _side
+
         ds, cfg = self.ds, self.cfg
         bound = ctypes.c_uint64()
         self._check(lib.gpzb_compress_bound(ds.count, ds.dims, ds.precision.value, cfg.block_size,
@@ -117,22 +119,33 @@ class _CudaHooks:
         args = (self.ptrs, ds.dims, ds.precision.value, ds.count, float(cfg.error_bound), cfg.eb_mode.value,
                 cfg.block_size, cfg.target_segs_per_axis, int(cfg.preserve_order), self.ws.data_ptr(),
                 self.ws.numel())
-        if cfg.eb_mode is not EbMode.RANGE_RELATIVE:  # per-block bounds still come from K1
-            self._check(lib.gpzb_range_async(self.ptrs, ds.dims, ds.precision.value, ds.count, cfg.block_size,
-                                             self.ws.data_ptr(), self.ws.numel(), self._stream()))
-        self._check(lib.gpzb_encode_plan_async(*args, self._stream()))
-        side_bytes, cta_b, warp_b = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
-        self._check(lib.gpzb_encode_plan_counts(self.ws.data_ptr(), self.ws.numel(), self._stream(),
-                                                ctypes.byref(side_bytes), ctypes.byref(cta_b), ctypes.byref(warp_b)))
-        side = torch.empty(max(side_bytes.value, 16), dtype=torch.uint8, device=self.axes[0].device)
-        e0 = self._ev() if self.timing is not None else None
-        self._check(lib.gpzb_encode_async(*args, side.data_ptr(), side_bytes.value, out.data_ptr(), bound.value,
-                                          0, ds.count, nb, 1, cta_b.value, warp_b.value, self._stream()))
-        if self.timing is not None:
-            self.timing.setdefault("encode", []).append((e0, self._ev()))
+        rel = cfg.eb_mode is EbMode.RANGE_RELATIVE
+        words = self.ws[40:56].view(torch.int64).clone() if rel else None  # the all-reduced range words
         res = _lib.Result()
-        st = lib.gpzb_compress_result(self.ws.data_ptr(), self.ws.numel(), ds.count, cfg.block_size,
-                                      self._stream(), ctypes.byref(res))
+
+        def run(first: bool) -> int:
+            if not first:  # a second pass after the side buffer grew (GPZB_NEED_SIDE)
+                self._check(lib.gpzb_workspace_reset_async(self.ws.data_ptr(), self.ws.numel(), ds.count,
+                                                           cfg.block_size, self._stream()))
+            if not first or not rel:  # per-block bounds come from K1 in both modes
+                self._check(lib.gpzb_range_async(self.ptrs, ds.dims, ds.precision.value, ds.count, cfg.block_size,
+                                                 self.ws.data_ptr(), self.ws.numel(), self._stream()))
+            if not first and rel:
+                self.ws[40:56].view(torch.int64).copy_(words)
+            self._check(lib.gpzb_encode_plan_async(*args, self._stream()))
+            side = _side(0)
+            e0 = self._ev() if (self.timing is not None and first) else None
+            self._check(lib.gpzb_encode_async(*args, side.data_ptr(), side.numel(), out.data_ptr(), bound.value,
+                                              0, ds.count, nb, 1, self._stream()))
+            if e0 is not None:
+                self.timing.setdefault("encode", []).append((e0, self._ev()))
+            return lib.gpzb_compress_result(self.ws.data_ptr(), self.ws.numel(), ds.count, cfg.block_size,
+                                            self._stream(), ctypes.byref(res))
+
+        st = run(True)
+        if st == _lib.NEED_SIDE:
+            _side(0, res.side_bytes)
+            st = run(False)
         return st, res, out[: res.out_len] if st == 0 else None
 
 
@@ -218,6 +231,7 @@ def compress_batch_device(datasets, cfg: CompressConfig, *, timing=None) -> list
             _allreduce_max_words(words)
             for j, w in zip(live, words):
                 j.ws[40:56].view(torch.int64).copy_(w)
+                j.words = w  # restored if the job encodes again (GPZB_NEED_SIDE)
         for i in range(k):
             _side_stream(i).wait_stream(cur)
     for i, j in enumerate(jobs):

@@ -37,3 +37,6 @@ def case(name):
 
 def error_prefix(msg: str) -> str:
     return msg.split(":")[0] if msg.startswith("block ") else ""
+
+with open(os.path.join(HERE, "stress.json")) as f:
+    STRESS = json.load(f)  # 1M UNIFORM_BOX / JITTERED_LATTICE goldens (tests/golden/make_golden_stress.py)

@@ -165,7 +165,7 @@ def test_nonfinite_abs_mode_detected_on_device():
 
 
 def test_sort_paths_are_all_exercised():
-    seen = np.zeros(6, np.int64)
+    seen = np.zeros(8, np.int64)
     for name in case_ids():
         (_, gen, count, dims, dt, eb, mode, bs, t, pres, seed, extra) = case(name)
         if GOLDEN["cases"][name]["error"] or count == 0:

@@ -95,3 +95,20 @@ def test_iter_blocks_matches_decompress():
     parts = list(O.iter_blocks(blob))
     for a in range(3):
         assert np.array_equal(np.concatenate([p[a] for p in parts]), full[a])
+
+
+@pytest.mark.parametrize("kind", ["uniform", "lattice"])
+def test_oracle_matches_reference_stress_fixtures(kind):
+    """1M-particle UNIFORM_BOX / JITTERED_LATTICE (SURVEY.md §8d stress
+    fixtures) at rel-eb 1e-2 / 1e-3 / 1e-4: container and reconstruction
+    SHA-256 of the reference itself (tests/golden/make_golden_stress.py)."""
+    from _golden import STRESS
+
+    gen = {"uniform": O.gen_uniform, "lattice": O.gen_lattice}[kind]
+    axes = gen(1_000_000, dims=3, seed=42)
+    want = STRESS[kind]
+    assert sha(*axes) == want["input_sha"]
+    for eb in (1e-2, 1e-3, 1e-4):
+        blob = O.compress(axes, O.Config(eb))
+        assert (len(blob), sha(blob)) == (want[repr(eb)]["container_len"], want[repr(eb)]["container_sha"])
+        assert sha(*O.decompress(blob)) == want[repr(eb)]["recon_sha"]
