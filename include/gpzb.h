@@ -147,12 +147,28 @@ int gpzb_encode_plan_async(const void* const* axes, int dims, int precision, uin
  *   table_base / header_count / header_blocks: sharding hooks — table entries
  *   are written as table_base + local prefix, and the global header (written
  *   when write_header != 0) names header_count particles in header_blocks
- *   blocks.  Single-GPU callers pass 0, count, ceil(count/bs), 1. */
+ *   blocks.  Single-GPU callers pass 0, count, ceil(count/bs), 1.
+ *   out == NULL: stop after the scan (K3a).  gpzb_compress_result then
+ *   reports the exact container size (out_len), and gpzb_emit_async writes
+ *   the container into a buffer of exactly that size — no bound-sized
+ *   allocation outlives the call. */
 int gpzb_encode_async(const void* const* axes, int dims, int precision, uint64_t count, double eb,
                       int eb_mode, uint32_t block_size, uint32_t target_segs_per_axis,
                       int preserve_order, void* ws, uint64_t ws_bytes, uint8_t* side,
                       uint64_t side_cap, uint8_t* out, uint64_t out_cap, uint64_t table_base,
                       uint64_t header_count, uint64_t header_blocks, int write_header, void* stream);
+
+/* K3b after gpzb_encode_async(out == NULL) and a successful
+ * gpzb_compress_result: offset table, global header (write_header != 0) and
+ * payload moves into `out`, whose capacity must be the out_len that
+ * gpzb_compress_result reported (the caller's claim; the payload total
+ * lives on the device).  `side` is the buffer given to gpzb_encode_async.
+ * Enqueued; no host synchronisation.  Replaces the concatenation step of
+ * container.compact / write_container (container.py:203-230). */
+int gpzb_emit_async(const void* const* axes, int dims, int precision, uint64_t count, double eb, int eb_mode,
+                    uint32_t block_size, int preserve_order, void* ws, uint64_t ws_bytes, const uint8_t* side,
+                    uint8_t* out, uint64_t out_cap, uint64_t table_base, uint64_t header_count,
+                    uint64_t header_blocks, int write_header, void* stream);
 
 /* Synchronise `stream` and read the result record of the last encode. */
 int gpzb_compress_result(void* ws, uint64_t ws_bytes, uint64_t count, uint32_t block_size,

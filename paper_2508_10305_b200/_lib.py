@@ -70,6 +70,8 @@ SIGNATURES = {
                                       _U64, _VP]),
     "gpzb_encode_async": (_I32, [ctypes.POINTER(_VP), _I32, _I32, _U64, _D, _I32, _U32, _U32, _I32, _VP, _U64,
                                  _VP, _U64, _VP, _U64, _U64, _U64, _U64, _I32, _VP]),
+    "gpzb_emit_async": (_I32, [ctypes.POINTER(_VP), _I32, _I32, _U64, _D, _I32, _U32, _I32, _VP, _U64, _VP, _VP,
+                               _U64, _U64, _U64, _U64, _I32, _VP]),
     "gpzb_compress_result": (_I32, [_VP, _U64, _U64, _U32, _VP, _RES]),
     "gpzb_compress": (_I32, [ctypes.POINTER(_VP), _I32, _I32, _U64, _D, _I32, _U32, _U32, _I32, _VP, _U64, _VP,
                              _U64, _VP, _RES]),

@@ -126,6 +126,51 @@ void clear_result(gpzb_result* r) {
   r->count_block = -1;
 }
 
+void set_out(EncParams& P, uint8_t* out, uint64_t nb, uint64_t table_base, uint64_t header_count,
+             uint64_t header_blocks, int write_header) {
+  P.header = out && write_header ? out : nullptr;
+  P.table0 = out ? out + GPZB_GLOBAL_HEADER_SIZE : nullptr;
+  P.table = out ? out + GPZB_GLOBAL_HEADER_SIZE + 8 : nullptr;
+  P.payload = out ? out + GPZB_GLOBAL_HEADER_SIZE + 8 * (nb + 1) : nullptr;
+  P.table_base = table_base;
+  P.header_count = header_count;
+  P.header_blocks = header_blocks;
+}
+
+// K3 parameters from the encoder's (payload == null: the container is not
+// allocated yet; K3a still runs, K3b waits for gpzb_emit_async).
+CompactParams make_compact(const EncParams& P, int dims, bool f64) {
+  CompactParams C;
+  memset(&C, 0, sizeof(C));
+  C.sizes = P.status;
+  C.tstat = P.tstat;
+  C.nblocks = P.nblocks;
+  C.table0 = P.table0;
+  C.table = P.table;
+  C.table_base = P.table_base;
+  C.res = P.res;
+  C.staging = P.staging;
+  C.side = P.side;
+  C.rec = P.rec;
+  C.payload = P.payload;
+  C.header = P.header;
+  C.dims = dims;
+  C.f64 = f64 ? 1 : 0;
+  C.preserve = P.preserve;
+  C.eb_mode_code = P.eb_mode_code;
+  C.eb = P.eb;
+  C.bs = P.bs;
+  C.header_count = P.header_count;
+  C.header_blocks = P.header_blocks;
+  return C;
+}
+
+// K3b: table entries, global header, payload moves.
+void launch_emit(const CompactParams& C, cudaStream_t s) {
+  GPZB_COUNT_LAUNCH();
+  k_copy_payloads<<<(unsigned)((C.nblocks + kCopyWarps - 1) / kCopyWarps), 32 * kCopyWarps, 0, s>>>(C);
+}
+
 template <int D, bool F64>
 void launch_range(const EncParams& P, cudaStream_t s) {
 #ifdef GPZB_K1_CTA
@@ -175,32 +220,10 @@ void launch_encode(const EncParams& P, cudaStream_t s) {
     GPZB_COUNT_LAUNCH();
     k_encode<D, F64><<<cgrid, kThreads, 0, s>>>(P);
   }
-  // K3: scan of the payload lengths, offset table, payload moves
-  CompactParams C;
-  C.sizes = P.status;
-  C.tstat = P.tstat;
-  C.nblocks = P.nblocks;
-  C.table0 = P.table0;
-  C.table = P.table;
-  C.table_base = P.table_base;
-  C.res = P.res;
-  C.staging = P.staging;
-  C.side = P.side;
-  C.rec = P.rec;
-  C.payload = P.payload;
-  C.header = P.header;
-  C.dims = D;
-  C.f64 = F64 ? 1 : 0;
-  C.preserve = P.preserve;
-  C.eb_mode_code = P.eb_mode_code;
-  C.eb = P.eb;
-  C.bs = P.bs;
-  C.header_count = P.header_count;
-  C.header_blocks = P.header_blocks;
   GPZB_COUNT_LAUNCH();
+  const CompactParams C = make_compact(P, D, F64);
   k_scan_sizes<<<(unsigned)((P.nblocks + kScanTile - 1) / kScanTile), kScanThreads, 0, s>>>(C);
-  GPZB_COUNT_LAUNCH();
-  k_copy_payloads<<<(unsigned)((P.nblocks + kCopyWarps - 1) / kCopyWarps), 32 * kCopyWarps, 0, s>>>(C);
+  if (P.payload) launch_emit(C, s);
 }
 
 template <int D, bool F64>
@@ -417,12 +440,15 @@ int gpzb_scan_sizes(const uint64_t* sizes, uint64_t nblocks, uint64_t* offsets, 
   C.sizes = sz;
   C.tstat = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(ws) + L.tstat);
   C.nblocks = nblocks;
-  C.table0 = reinterpret_cast<uint8_t*>(offsets);
-  C.table = reinterpret_cast<uint8_t*>(offsets + 1);
   C.res = reinterpret_cast<DevResult*>(ws);
   GPZB_COUNT_LAUNCH();
   k_scan_sizes<<<(unsigned)((nblocks + kScanTile - 1) / kScanTile), kScanThreads, 0, s>>>(C);
-  return cuda_status(cudaGetLastError());
+  e = cudaGetLastError();
+  // exclusive offsets (in place in the workspace), then the total
+  if (e == cudaSuccess) e = cudaMemcpyAsync(offsets, sz, 8 * nblocks, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(offsets + nblocks, &C.res->total_payload, 8, cudaMemcpyDeviceToDevice, s);
+  return cuda_status(e);
 }
 
 const char* gpzb_version(void) { return "gpzb 0.1 sm_100a"; }
@@ -560,7 +586,7 @@ int gpzb_encode_async(const void* const* axes, int dims, int prec, uint64_t coun
   if (ws_bytes < enc_layout(nb, dims, prec).total) return GPZB_INVALID_ARGUMENT;
   uint64_t bound = 0;
   gpzb_compress_bound(count, dims, prec, bs, target, pres, &bound);
-  if (out_cap < bound) return GPZB_INVALID_ARGUMENT;
+  if (out && out_cap < bound) return GPZB_INVALID_ARGUMENT;
   if (nb == 0) return GPZB_OK;
   EncParams P = make_enc(axes, dims, prec, count, bs, ws);
   P.target = target;
@@ -570,14 +596,28 @@ int gpzb_encode_async(const void* const* axes, int dims, int prec, uint64_t coun
   P.preserve = pres != 0;
   P.side = side;
   P.side_cap = side ? side_cap : 0;
-  P.header = write_header ? out : nullptr;
-  P.table0 = out + GPZB_GLOBAL_HEADER_SIZE;
-  P.table = out + GPZB_GLOBAL_HEADER_SIZE + 8;
-  P.payload = out + GPZB_GLOBAL_HEADER_SIZE + 8 * (nb + 1);
-  P.table_base = table_base;
-  P.header_count = header_count;
-  P.header_blocks = header_blocks;
+  set_out(P, out, nb, table_base, header_count, header_blocks, write_header);
   DISPATCH_DP(dims, prec, launch_encode, P, (cudaStream_t)stream);
+  return cuda_status(cudaGetLastError());
+}
+
+int gpzb_emit_async(const void* const* axes, int dims, int prec, uint64_t count, double eb, int eb_mode,
+                    uint32_t bs, int pres, void* ws, uint64_t ws_bytes, const uint8_t* side, uint8_t* out,
+                    uint64_t out_cap, uint64_t table_base, uint64_t header_count, uint64_t header_blocks,
+                    int write_header, void* stream) {
+  int st = check_args(dims, prec, bs);
+  if (st) return st;
+  const uint64_t nb = nblocks_of(count, bs);
+  if (ws_bytes < enc_layout(nb, dims, prec).total) return GPZB_INVALID_ARGUMENT;
+  if (!out || out_cap < GPZB_GLOBAL_HEADER_SIZE + 8 * (nb + 1)) return GPZB_INVALID_ARGUMENT;
+  if (nb == 0) return GPZB_OK;
+  EncParams P = make_enc(axes, dims, prec, count, bs, ws);
+  P.eb = eb;
+  P.eb_mode_code = eb_mode;
+  P.preserve = pres != 0;
+  P.side = const_cast<uint8_t*>(side);
+  set_out(P, out, nb, table_base, header_count, header_blocks, write_header);
+  launch_emit(make_compact(P, dims, prec == GPZB_F64), (cudaStream_t)stream);
   return cuda_status(cudaGetLastError());
 }
 

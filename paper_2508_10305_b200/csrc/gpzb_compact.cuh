@@ -8,12 +8,15 @@
 //   K3a k_scan_sizes     single-pass decoupled look-back scan over the
 //                        payload lengths (tiles of 8192 blocks; each tile
 //                        publishes its aggregate, warp 0 looks back over the
-//                        tile words): exclusive offsets in place, the u64 LE
-//                        offset table, the total payload length
-//   K3b k_copy_payloads  one warp per block: the payload moved from its slot
-//                        to its byte offset (arbitrary alignment) with
-//                        funnel-shifted 16-byte stores; edge chunks shared
-//                        with the neighbouring payloads use narrower stores
+//                        tile words): exclusive offsets in place and the
+//                        total payload length (the container size is known
+//                        here, so the caller can allocate it exactly)
+//   K3b k_copy_payloads  one warp per block: its u64 LE offset-table entry,
+//                        and the payload moved from its slot to its byte
+//                        offset (arbitrary alignment) with funnel-shifted
+//                        16-byte stores; edge chunks shared with the
+//                        neighbouring payloads use narrower stores; block 0
+//                        also writes table entry 0 and the global header
 //
 // This is the paper's three-step compaction, with the
 // prefix sum done as a single-pass look-back scan.  Keeping the look-back
@@ -135,19 +138,15 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_sizes(const CompactParams
   }
   __syncthreads();
   unsigned long long run = tile_excl + warp_tot[wid] + x - sum;
-  const bool even = ((uintptr_t)P.table & 1) == 0;
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
     const uint64_t b = first + i;
     if (b < P.nblocks) {
       P.sizes[b] = run;
       run += v[i];
-      put_u64_le(P.table + 8 * b, P.table_base + run, even);
       if (b + 1 == P.nblocks) P.res->total_payload = run;
     }
   }
-  if (tile == 0 && tid == 0 && P.table0) put_u64_le(P.table0, P.table_base, false);
-  if (tile == 0 && tid == 32 && P.header) write_global_header(P);
 }
 
 // Move `len` payload bytes from a 16-byte aligned slot to dst (any
@@ -206,6 +205,10 @@ __global__ void __launch_bounds__(32 * kCopyWarps) k_copy_payloads(const Compact
   const uint64_t ex = P.sizes[blk];
   const uint64_t end = (blk + 1 < P.nblocks) ? P.sizes[blk + 1] : P.res->total_payload;
   const uint32_t len = (uint32_t)(end - ex);
+  // this block's offset-table entry (write_container, container.py:211-230)
+  if (lane == 0) put_u64_le(P.table + 8 * blk, P.table_base + end, ((uintptr_t)P.table & 1) == 0);
+  if (blk == 0 && lane == 1 && P.table0) put_u64_le(P.table0, P.table_base, false);
+  if (blk == 0 && lane == 2 && P.header) write_global_header(P);
   if (len == 0) return;
   const uint8_t kind = P.rec[blk].kind;
   const uint8_t* src = kind == KIND_WIDE ? P.side + P.rec[blk].side_off : P.staging + blk * (uint64_t)kSlotBytes;

@@ -128,15 +128,38 @@ def pair_blocks(original: Dataset, reconstructed: Dataset, cfg: CompressConfig,
     return oi.cpu().numpy(), ri.cpu().numpy()
 
 
+def _index_array(idx, size: int) -> torch.Tensor:
+    """A pairing index vector on the device with numpy's fancy-indexing rules
+    (metrics.py:93-94): negative indices count from the end, anything outside
+    [-size, size) raises IndexError."""
+    t = _dev_array(idx, torch.int64)
+    if t.numel():
+        lo, hi = int(t.min()), int(t.max())
+        if lo < -size or hi >= size:
+            bad = lo if lo < -size else hi
+            raise IndexError(f"index {bad} is out of bounds for axis 0 with size {size}")
+        if lo < 0:
+            t = torch.where(t < 0, t + size, t)
+    return t
+
+
 def _stats(orig: list, rec: list, pairing, eb_abs: float, want_violations: bool):
     """K5b over paired values: (stats vector, violations array [k, 3] or None)."""
     dims = len(orig)
-    n = int(orig[0].numel())
-    ws = _pair_ws(n, dims)
+    n_o, n_r = int(orig[0].numel()), int(rec[0].numel())
     oi = ri = None
-    if pairing is not None:
-        oi = _dev_array(pairing[0], torch.int64)
-        ri = _dev_array(pairing[1], torch.int64)
+    if pairing is None:
+        # elementwise o - r: numpy broadcasting rejects unequal lengths (metrics.py:90-97)
+        if n_o != n_r:
+            raise ValueError(f"operands could not be broadcast together with shapes ({n_o},) ({n_r},)")
+        n = n_o
+    else:
+        oi = _index_array(pairing[0], n_o)
+        ri = _index_array(pairing[1], n_r)
+        if oi.numel() != ri.numel():
+            raise ValueError(f"operands could not be broadcast together with shapes ({oi.numel()},) ({ri.numel()},)")
+        n = int(oi.numel())
+    ws = _pair_ws(n, dims)
     stats = (ctypes.c_double * (1 + 3 * dims))()
     count = ctypes.c_uint64()
     cap = 4096 if want_violations else 0

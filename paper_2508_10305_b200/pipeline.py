@@ -173,7 +173,7 @@ def _compress_begin(ds, cfg: CompressConfig, slot: int, timing, plan: bool = Tru
     _check(lib.gpzb_compress_bound(j.count, j.dims, j.prec, j.bs, j.t, j.pres, ctypes.byref(bound)))
     j.bound = bound.value
     j.ws = _workspace(ws_bytes.value, slot)
-    j.out = torch.empty(j.bound, dtype=torch.uint8, device=j.axes[0].device)
+    j.out = None  # allocated at its exact size once the scan has run (_compress_finish)
     j.ptrs = _lib.ptr_array([a.data_ptr() for a in j.axes])
     j.res = _lib.Result()
     j.stream = _stream()
@@ -205,10 +205,25 @@ def _compress_encode(j: _Job) -> None:
     side = _side(j.slot)
     e0 = _ev() if j.timing is not None else None
     _check(lib.gpzb_encode_async(j.ptrs, j.dims, j.prec, j.count, j.eb, j.mode, j.bs, j.t, j.pres, j.ws.data_ptr(),
-                                 j.ws.numel(), side.data_ptr(), side.numel(), j.out.data_ptr(), j.bound, 0,
+                                 j.ws.numel(), side.data_ptr(), side.numel(), None, 0, 0,
                                  j.count, j.nb, 1, j.stream))
     if j.timing is not None:
-        j.timing.setdefault("encode", []).append((e0, _ev()))
+        j.timing.setdefault("encode", []).append((e0, None))
+
+
+def _compress_emit(j: _Job, table_base: int = 0, header_count=None, header_blocks=None,
+                   write_header: int = 1) -> torch.Tensor:
+    """After a successful result read: allocate the container at its exact
+    size and enqueue K3b (offset table, header, payload moves) into it."""
+    j.out = torch.empty(j.res.out_len, dtype=torch.uint8, device=j.axes[0].device)
+    side = _side(j.slot)
+    _check(lib.gpzb_emit_async(j.ptrs, j.dims, j.prec, j.count, j.eb, j.mode, j.bs, j.pres, j.ws.data_ptr(),
+                               j.ws.numel(), side.data_ptr(), j.out.data_ptr(), j.out.numel(), table_base,
+                               j.count if header_count is None else header_count,
+                               j.nb if header_blocks is None else header_blocks, write_header, j.stream))
+    if j.timing is not None and j.timing.get("encode") and j.timing["encode"][-1][1] is None:
+        j.timing["encode"][-1] = (j.timing["encode"][-1][0], _ev())
+    return j.out
 
 
 def _compress_status(j: _Job) -> int:
@@ -217,6 +232,7 @@ def _compress_status(j: _Job) -> int:
     wrote nothing for them and reports the size: grow it and encode again
     (the range words of a sharded run are restored from j.words)."""
     if j.count == 0:
+        j.out = torch.empty(j.bound, dtype=torch.uint8, device=j.axes[0].device)
         return lib.gpzb_compress(j.ptrs, j.dims, j.prec, j.count, j.eb, j.mode, j.bs, j.t, j.pres, j.ws.data_ptr(),
                                  j.ws.numel(), j.out.data_ptr(), j.bound, j.stream, ctypes.byref(j.res))
     st = lib.gpzb_compress_result(j.ws.data_ptr(), j.ws.numel(), j.count, j.bs, j.stream, ctypes.byref(j.res))
@@ -242,7 +258,9 @@ def _compress_finish(j: _Job) -> torch.Tensor:
     _check(st, j.res)
     compress_device.last_result = j.res
     _tls("last").update(ws=j.ws, count=j.count, bs=j.bs, dims=j.dims, prec=j.prec)
-    return j.out[: j.res.out_len]
+    if j.count == 0:
+        return j.out[: j.res.out_len].clone()
+    return _compress_emit(j)
 
 
 def last_path_counts() -> list:
@@ -519,6 +537,11 @@ def _streamed_plan(host: np.ndarray, h: _lib.Header):
     n = host.size
     if (nb < 2 or h.particle_count == 0 or n < (32 << 20) or h.table_end + h.payload_len != n
             or h.block_size > _lib.MAX_BLOCK_SIZE):
+        return None
+    # the output buffers are sized from particle_count: only trust it when it
+    # agrees with the block count (else the one-shot decode reports the
+    # reference's "block i: ... boundary" error, pipeline.py:174-181)
+    if not (nb - 1) * h.block_size < h.particle_count <= nb * h.block_size:
         return None
     tab = host[_lib.GLOBAL_HEADER_SIZE: _lib.GLOBAL_HEADER_SIZE + 8 * (nb + 1)].view("<u8")
     if int(tab[0]) != 0 or int(tab[-1]) != h.payload_len or bool(np.any(tab[1:] < tab[:-1])):

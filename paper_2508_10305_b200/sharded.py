@@ -107,21 +107,28 @@ class _CudaHooks:
         return self.ws[40:56].view(torch.int64)  # DevResult.range_w, in place
 
     def local_encode(self, global_count: int, global_blocks: int):
+        """This rank's local container (a valid .gpz of its own blocks),
+        allocated at its exact size after the scan; an empty shard gets the
+        empty container (header + entry 0)."""
         from .pipeline import _side
 
         ds, cfg = self.ds, self.cfg
-        bound = ctypes.c_uint64()
-        self._check(lib.gpzb_compress_bound(ds.count, ds.dims, ds.precision.value, cfg.block_size,
-                                            cfg.target_segs_per_axis, int(cfg.preserve_order),
-                                            ctypes.byref(bound)))
-        out = torch.empty(bound.value, dtype=torch.uint8, device=self.axes[0].device)
-        nb = (ds.count + cfg.block_size - 1) // cfg.block_size
+        dev = self.axes[0].device if self.axes else torch.device("cuda", torch.cuda.current_device())
+        res = _lib.Result()
         args = (self.ptrs, ds.dims, ds.precision.value, ds.count, float(cfg.error_bound), cfg.eb_mode.value,
                 cfg.block_size, cfg.target_segs_per_axis, int(cfg.preserve_order), self.ws.data_ptr(),
                 self.ws.numel())
+        if ds.count == 0:
+            bound = ctypes.c_uint64()
+            self._check(lib.gpzb_compress_bound(0, ds.dims, ds.precision.value, cfg.block_size,
+                                                cfg.target_segs_per_axis, int(cfg.preserve_order),
+                                                ctypes.byref(bound)))
+            out = torch.empty(bound.value, dtype=torch.uint8, device=dev)
+            st = lib.gpzb_compress(*args, out.data_ptr(), bound.value, self._stream(), ctypes.byref(res))
+            return st, res, out[: res.out_len].clone() if st == 0 else None
+        nb = (ds.count + cfg.block_size - 1) // cfg.block_size
         rel = cfg.eb_mode is EbMode.RANGE_RELATIVE
         words = self.ws[40:56].view(torch.int64).clone() if rel else None  # the all-reduced range words
-        res = _lib.Result()
 
         def run(first: bool) -> int:
             if not first:  # a second pass after the side buffer grew (GPZB_NEED_SIDE)
@@ -134,19 +141,40 @@ class _CudaHooks:
                 self.ws[40:56].view(torch.int64).copy_(words)
             self._check(lib.gpzb_encode_plan_async(*args, self._stream()))
             side = _side(0)
-            e0 = self._ev() if (self.timing is not None and first) else None
-            self._check(lib.gpzb_encode_async(*args, side.data_ptr(), side.numel(), out.data_ptr(), bound.value,
-                                              0, ds.count, nb, 1, self._stream()))
-            if e0 is not None:
-                self.timing.setdefault("encode", []).append((e0, self._ev()))
+            self._check(lib.gpzb_encode_async(*args, side.data_ptr(), side.numel(), None, 0, 0, ds.count, nb, 1,
+                                              self._stream()))
             return lib.gpzb_compress_result(self.ws.data_ptr(), self.ws.numel(), ds.count, cfg.block_size,
                                             self._stream(), ctypes.byref(res))
 
+        e0 = self._ev() if self.timing is not None else None
         st = run(True)
         if st == _lib.NEED_SIDE:
             _side(0, res.side_bytes)
             st = run(False)
-        return st, res, out[: res.out_len] if st == 0 else None
+        if st != 0:
+            return st, res, None
+        out = torch.empty(res.out_len, dtype=torch.uint8, device=dev)
+        self._check(lib.gpzb_emit_async(self.ptrs, ds.dims, ds.precision.value, ds.count, float(cfg.error_bound),
+                                        cfg.eb_mode.value, cfg.block_size, int(cfg.preserve_order),
+                                        self.ws.data_ptr(), self.ws.numel(), _side(0).data_ptr(), out.data_ptr(),
+                                        out.numel(), 0, ds.count, nb, 1, self._stream()))
+        if e0 is not None:
+            self.timing.setdefault("encode", []).append((e0, self._ev()))
+        return st, res, out
+
+
+def _eb_bits(v: float) -> int:
+    return struct.unpack("<q", struct.pack("<d", float(v)))[0]
+
+
+def _global_eb_abs(cfg: CompressConfig, rows: list) -> float:
+    """The header's eb_abs: every non-empty rank resolved the same value from
+    the all-reduced range words, so take the first one's; a dataset with no
+    particles at all keeps the raw bound (pipeline.py:75)."""
+    for r in rows:
+        if r["count"] > 0:
+            return struct.unpack("<d", struct.pack("<q", r["eb_bits"]))[0]
+    return float(cfg.error_bound)
 
 
 def _header(dims, prec, cfg: CompressConfig, eb_abs: float, count: int, blocks: int) -> bytes:
@@ -170,24 +198,26 @@ def compress_device(ds: Dataset, cfg: CompressConfig, *, timing=None, hooks=None
         words = h.local_range_words()
         _allreduce_max_words(words)
     st, res, local = h.local_encode(g_count, g_blocks)
-    # the first error over ranks in global block order (pipeline.py:80-83);
-    # dataset-level errors (non-finite input) precede every block error
+    # one all-gather: the first error over ranks in global block order
+    # (pipeline.py:80-83; dataset-level errors precede every block error),
+    # each rank's payload total (-> its base offset) and its resolved eb_abs
     inf = 1 << 62
+    nb = (ds.count + bs - 1) // bs
     key = inf if st == 0 else (-1 if res.block < 0 else first_block + res.block)
-    info = torch.tensor([key, st, res.reason, res.axis], dtype=torch.int64, device=_comm_device())
+    payload = (int(local.numel() if hasattr(local, "numel") else len(local)) - 46 - 8 * (nb + 1)) if st == 0 else 0
+    info = torch.tensor([key, st, res.reason, res.axis, payload, _eb_bits(res.eb_abs), ds.count],
+                        dtype=torch.int64, device=_comm_device())
     allinfo = [torch.zeros_like(info) for _ in range(world)]
     dist.all_gather(allinfo, info)
-    win = min(allinfo, key=lambda t: int(t[0]))
-    if int(win[0]) != inf:
+    rows = [dict(zip(("key", "st", "reason", "axis", "payload", "eb_bits", "count"), t.tolist())) for t in allinfo]
+    win = min(rows, key=lambda r: r["key"])
+    if win["key"] != inf:
         from .pipeline import _check
 
-        k, wst, wreason, waxis = (int(x) for x in win)
-        _check(wst, _lib.Result(status=wst, reason=wreason, block=k, axis=waxis))
-    nb = (ds.count + bs - 1) // bs
-    payload = int(local.numel() if hasattr(local, "numel") else len(local)) - 46 - 8 * (nb + 1)
-    totals = _gather_ints(payload, _comm_device())
+        _check(win["st"], _lib.Result(status=win["st"], reason=win["reason"], block=win["key"], axis=win["axis"]))
+    totals = [r["payload"] for r in rows]
     base = sum(totals[:rank])
-    header = _header(ds.dims, ds.precision.value, cfg, float(res.eb_abs), g_count, g_blocks)
+    header = _header(ds.dims, ds.precision.value, cfg, _global_eb_abs(cfg, rows), g_count, g_blocks)
     return ShardedContainer(local=local, rank=rank, world=world, base=base, first_block=first_block,
                             global_count=g_count, global_blocks=g_blocks, local_blocks=nb, header=header,
                             global_payload=sum(totals))
@@ -199,7 +229,8 @@ def compress_batch_device(datasets, cfg: CompressConfig, *, timing=None) -> list
     ONE collective per exchange for all of them: the shard counts, the range
     words (REL), and the (first error, payload total) records.  Returns one
     ShardedContainer per dataset, each identical to compress_device's."""
-    from .pipeline import _check, _compress_begin, _compress_encode, _compress_plan, _compress_status, _side_stream
+    from .pipeline import (_check, _compress_begin, _compress_emit, _compress_encode, _compress_plan, _compress_status,
+                           _side_stream)
 
     rank, world = dist.get_rank(), dist.get_world_size()
     bs = cfg.block_size
@@ -245,14 +276,19 @@ def compress_batch_device(datasets, cfg: CompressConfig, *, timing=None) -> list
     for i, j in enumerate(jobs):
         with torch.cuda.stream(_side_stream(i)):
             st = _compress_status(j)
+            if st != 0:
+                local = None
+            elif j.count == 0:
+                local = j.out[: j.res.out_len].clone()  # the empty local container
+            else:
+                local = _compress_emit(j)
         cur.wait_stream(_side_stream(i))
         first_block = sum((c[i] + bs - 1) // bs for c in counts[:rank])
         key = inf if st == 0 else (-1 if j.res.block < 0 else first_block + j.res.block)
-        local = j.out[: j.res.out_len] if st == 0 else None
         if local is not None:
             local.record_stream(cur)
         payload = (int(local.numel()) - 46 - 8 * (j.nb + 1)) if local is not None else 0
-        rows.append([key, st, j.res.reason, j.res.axis, payload])
+        rows.append([key, st, j.res.reason, j.res.axis, payload, _eb_bits(j.res.eb_abs), j.count])
         locals_.append(local)
     info = torch.tensor(rows, dtype=torch.int64, device=dev)
     alli = [torch.zeros_like(info) for _ in range(world)]
@@ -262,12 +298,13 @@ def compress_batch_device(datasets, cfg: CompressConfig, *, timing=None) -> list
     for i, (ds, j) in enumerate(zip(datasets, jobs)):
         win = min((alli[r][i] for r in range(world)), key=lambda v: v[0])
         if win[0] != inf:
-            key, wst, wreason, waxis, _ = win
+            key, wst, wreason, waxis = win[:4]
             _check(wst, _lib.Result(status=wst, reason=wreason, block=key, axis=waxis))
         totals = [alli[r][i][4] for r in range(world)]
         g_count = sum(c[i] for c in counts)
         g_blocks = sum((c[i] + bs - 1) // bs for c in counts)
-        header = _header(ds.dims, ds.precision.value, cfg, float(j.res.eb_abs), g_count, g_blocks)
+        eb_abs = _global_eb_abs(cfg, [{"count": alli[r][i][6], "eb_bits": alli[r][i][5]} for r in range(world)])
+        header = _header(ds.dims, ds.precision.value, cfg, eb_abs, g_count, g_blocks)
         out.append(ShardedContainer(local=locals_[i], rank=rank, world=world, base=sum(totals[:rank]),
                                     first_block=sum((c[i] + bs - 1) // bs for c in counts[:rank]),
                                     global_count=g_count, global_blocks=g_blocks, local_blocks=j.nb,

@@ -31,29 +31,17 @@ def _cuda():
 
 
 def gen_lidar(n: int, seed: int):
-    """2.5-D terrain in scan-line order: jittered x/y lattice rows, z a smooth
-    height field plus sensor noise."""
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    w = int(np.ceil(np.sqrt(n)))
-    i = torch.arange(n, device="cuda", dtype=torch.int64)
-    f64 = torch.float64
-    x = (i % w).to(f64) * 0.05 + (torch.rand(n, generator=g, device="cuda", dtype=f64) * 2 - 1) * 0.01
-    y = (i // w).to(f64) * 0.05 + (torch.rand(n, generator=g, device="cuda", dtype=f64) * 2 - 1) * 0.01
-    z = 10.0 * torch.sin(x / 50.0) * torch.cos(y / 37.0) + 0.002 * torch.randn(n, generator=g, device="cuda",
-                                                                                  dtype=f64)
-    return [x.float(), y.float(), z.float()]
+    """bench.py's configs[2] generator (the benchmarked data is the tested data)."""
+    import bench
+
+    return bench.gen_lidar(n, seed, torch.device("cuda"))
 
 
 def gen_clusters_dev(n: int, clusters: int, sigma: float, seed: int):
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    centers = torch.rand(clusters, 3, generator=g, device="cuda", dtype=torch.float64)
-    out = []
-    for a in range(3):
-        assign = (torch.arange(n, device="cuda", dtype=torch.int64) * clusters) // n
-        v = centers[assign, a] + sigma * torch.randn(n, generator=g, device="cuda", dtype=torch.float64)
-        del assign
-        out.append(v.float())
-    return out
+    """bench.py's configs[3] generator."""
+    import bench
+
+    return bench.gen_clusters(n, clusters, sigma, seed, torch.device("cuda"))
 
 
 def sampled_parity(axes, cfg, container, rec, picks):

@@ -160,3 +160,26 @@ def test_gpu_nrmse_unpaired_and_device_inputs():
     with pytest.raises(gz.DomainError, match="degenerate field range"):
         M.nrmse(np.ones(10), np.ones(10) * 2)
     assert M.aggregate_psnr([0.0, 0.0]) == math.inf
+
+
+@gpu
+def test_gpu_nrmse_rejects_mismatched_inputs_like_numpy():
+    """Unequal lengths and out-of-range / short pairings raise like the
+    reference's numpy indexing (metrics.py:90-97) instead of reading past a
+    buffer; negative indices count from the end."""
+    _gz()
+    from paper_2508_10305_b200 import metrics as M
+
+    rng = np.random.default_rng(6)
+    a = rng.normal(size=1000)
+    b = a + rng.normal(scale=1e-3, size=a.size)
+    with pytest.raises(ValueError):
+        M.nrmse(a, b[:999])
+    with pytest.raises(ValueError):
+        M.nrmse(a, b, (np.arange(10), np.arange(9)))
+    with pytest.raises(IndexError):
+        M.nrmse(a, b, (np.arange(10), np.arange(10) + 995))
+    p = (np.array([-1, 3, 5]), np.array([999, -997, 5]))
+    assert math.isclose(M.nrmse(a, b, p), O.nrmse(a, b, p), rel_tol=RTOL)
+    p = (np.arange(500), np.arange(500))
+    assert math.isclose(M.nrmse(a, b, p), O.nrmse(a, b, p), rel_tol=RTOL)

@@ -145,3 +145,40 @@ def test_mixed_signed_zero_bounds_pinned():
         assert got[d] ^ want[d] == 0x80  # its sign bit, nothing else
     for a, b, c in zip(gz.decompress(got).axes, O.decompress(want), O.decompress(got)):
         assert np.array_equal(a, b) and np.array_equal(b, c)
+
+
+def test_concurrent_threads_get_their_own_results():
+    """compress / decompress from several host threads at once, on distinct
+    data (safe for concurrent calls): every thread's bytes and
+    values equal the sequential results (per-thread workspaces, pinned
+    buffers and side buffers, pipeline._tls)."""
+    import threading
+
+    sets = [O.gen_clusters(300_000 + 1000 * k, dims=3, seed=40 + k) for k in range(4)]
+    cfg = gz.CompressConfig(error_bound=1e-3)
+    want = [gz.compress(gz.Dataset.from_axes(a), cfg) for a in sets]
+    want_dev = [gz.compress_device(gz.Dataset.from_axes([torch.from_numpy(x).cuda() for x in a]), cfg).cpu()
+                for a in sets]
+    errs = []
+
+    def work(k):
+        try:
+            ds = gz.Dataset.from_axes(sets[k])
+            dsd = gz.Dataset.from_axes([torch.from_numpy(x).cuda() for x in sets[k]])
+            for _ in range(6):
+                blob = gz.compress(ds, cfg)
+                assert blob == want[k], k
+                rec = gz.decompress(blob)
+                ref = O.decompress(want[k])
+                assert all(np.array_equal(a, b) for a, b in zip(rec.axes, ref)), k
+                c = gz.compress_device(dsd, cfg)
+                assert torch.equal(c.cpu(), want_dev[k]), k
+        except Exception as exc:  # noqa: BLE001
+            errs.append((k, repr(exc)))
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs

@@ -37,6 +37,9 @@ class OracleHooks:
         self.axes, self.cfg = axes, cfg
 
     def local_range_words(self):
+        if self.axes[0].size == 0:  # an empty shard: the zeroed words (below every key)
+            self.words = torch.zeros(2, dtype=torch.int64)
+            return self.words
         lo = min(float(a.min()) for a in self.axes)
         hi = max(float(a.max()) for a in self.axes)
         self.words = torch.tensor([_ukey(-lo), _ukey(hi)], dtype=torch.int64)
@@ -46,6 +49,10 @@ class OracleHooks:
         import paper_2508_10305_b200._lib as L
 
         c = self.cfg
+        if self.axes[0].size == 0:
+            blob = O.assemble(len(self.axes), O.F32, O.Config(c.error_bound, c.eb_mode.value, c.block_size), 0.0,
+                              0, [])
+            return 0, L.Result(status=0, eb_abs=0.0), blob
         if c.eb_mode.value == O.RANGE_RELATIVE:
             lo, hi = -_ukey_inv(int(self.words[0])), _ukey_inv(int(self.words[1]))
             span = hi - lo
@@ -79,7 +86,7 @@ def _run(rank, world, port, case, q, path=None):
         if case == "overflow":
             full[0] = full[0].astype(np.float32)
             full[0][3500] = 3e38  # block 3 (rank 1's first block) overflows in ABS mode
-        cuts = [0, 3072, 5000]
+        cuts = [0, 0, 5000] if case == "empty" else [0, 3072, 5000]  # "empty": rank 0 holds no particles
         local = [a[cuts[rank]:cuts[rank + 1]] for a in full]
         mode = gz.EbMode.ABSOLUTE if case == "overflow" else gz.EbMode.RANGE_RELATIVE
         cfg = gz.CompressConfig(error_bound=1e-3 if case != "overflow" else 1e-6, eb_mode=mode)
@@ -119,7 +126,7 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("case", ["rel", "overflow", "file"])
+@pytest.mark.parametrize("case", ["rel", "overflow", "file", "empty"])
 def test_sharded_global_container_equals_single_process(case, tmp_path):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -132,7 +139,7 @@ def test_sharded_global_container_equals_single_process(case, tmp_path):
     for p in procs:
         p.join(timeout=60)
     out.sort()
-    if case in ("rel", "file"):
+    if case in ("rel", "file", "empty"):
         assert out[0][1:3] == ("ok", True), out
         assert out[1][1] == "ok"
     else:
@@ -172,6 +179,17 @@ def _run_cuda(rank, world, port, q, path):
             full_rec = gz.decompress(gz.compress(gz.Dataset.from_axes(full), cfg))
             ok_rec = all(np.array_equal(r.cpu().numpy(), w[cut:]) for r, w in zip(rec.axes, full_rec.axes))
             q.put((rank, True, True, ok_rec))
+        # an empty shard on rank 0: its local container is the valid empty
+        # one and the global header carries rank 1's eb_abs
+        sl = slice(0, 0) if rank == 0 else slice(0, None)
+        ds = gz.Dataset.from_axes([torch.from_numpy(a[sl].copy()).cuda() for a in full])
+        sc = sharded.compress_device(ds, cfg)
+        blob = sharded.to_global_bytes(sc)
+        assert gz.decompress_device(sc.local).count == ds.count
+        if rank == 0:
+            q.put((rank + 10, blob == want, True, True))
+        else:
+            q.put((rank + 10, True, True, True))
     finally:
         dist.destroy_process_group()
 
@@ -187,10 +205,10 @@ def test_sharded_cuda_hooks_two_ranks_one_gpu(tmp_path):
     procs = [ctx.Process(target=_run_cuda, args=(r, 2, port, q, path)) for r in range(2)]
     for p in procs:
         p.start()
-    out = sorted(q.get(timeout=300) for _ in procs)
+    out = sorted(q.get(timeout=300) for _ in range(2 * len(procs)))
     for p in procs:
         p.join(timeout=60)
-    assert out == [(0, True, True, True), (1, True, True, True)], out
+    assert out == [(0, True, True, True), (1, True, True, True), (10, True, True, True), (11, True, True, True)], out
 
 
 def _run_cuda_batch(rank, world, port, q):

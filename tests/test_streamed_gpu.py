@@ -111,6 +111,14 @@ def test_streamed_errors_match_one_shot(blob):
     o = 46 + 8 * (nb // 2)
     b4[o: o + 8] = (h.payload_len + 1).to_bytes(8, "little")
     cases.append(bytes(b4))
+    # a corrupted particle count (high bits of header bytes 30-37): no
+    # terabyte-sized pinned buffers, the reference's boundary error
+    b5 = bytearray(blob)
+    b5[36] ^= 0x40
+    cases.append(bytes(b5))
+    b6 = bytearray(blob)
+    b6[30:38] = (h.particle_count + 5000).to_bytes(8, "little")
+    cases.append(bytes(b6))
     for c in cases:
         e_stream = _err(lambda: gz.decompress(c))
         e_dev = _err(lambda: _one_shot(c))

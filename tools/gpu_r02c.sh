@@ -1,0 +1,18 @@
+#!/bin/bash
+# Round-2 check: GPU tests, smoke, bench of every workload, traffic capture.
+cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
+mkdir -p gpurun_out
+tag=${1:-r02c}
+free -g > gpurun_out/${tag}_free.txt; nproc >> gpurun_out/${tag}_free.txt
+timeout 1500 python -m pytest tests -q -m gpu --durations=15 > gpurun_out/${tag}_pytest.txt 2>&1
+echo "pytest rc=$?" >> gpurun_out/${tag}_pytest.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${tag}_smoke.txt 2>&1
+timeout 900 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
+for w in lidar500m decomp1b snapshot2b; do
+  timeout 900 python bench.py --workload $w --steps 5 --warmup 3 > gpurun_out/${tag}_bench_$w.json 2> gpurun_out/${tag}_bench_$w.err
+done
+timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/${tag}_traffic_hacc.csv python bench.py --per-call --steps 1 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches.csv \
+    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
+ls -la gpurun_out | grep $tag
