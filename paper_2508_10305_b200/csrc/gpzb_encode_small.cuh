@@ -74,11 +74,13 @@ struct SmallSmem {
       uint8_t soff[kMaxBs];              // offsets in (seg, off) order
     } o;
   } u;
-  // per segment rank: two words of 8 nibble counters by offset (or the count)
+  // per segment rank r: counter word(s), at cnt[h * 1024 + (r & 7) * 128 + (r >> 3)]
+  // (h = off >> 3) so that thread t's runs 8t..8t+7 are conflict-free
   __align__(16) uint32_t cnt[HAS_OFF ? 2 * kMaxBs : kMaxBs];
   __align__(16) uint16_t uniq[kMaxBs + 8];  // [0] = 0 sentinel, [r + 1] = unique id of rank r
 };
 static_assert(kSmallStageWords <= kSmallMaxPN / 32, "the stage reuses the bitmap");
+__device__ __forceinline__ uint32_t cnt_idx(uint32_t r) { return ((r & 7u) << 7) | (r >> 3); }
 
 // Exclusive scan of one value per thread over the (kSW-warp) CTA with a
 // single barrier.  `ws` (16-byte aligned) is not rewritten before a later
@@ -187,6 +189,7 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
 #pragma unroll
       for (int a = 0; a < D; ++a) {
         const double lo = rec.lo[a], rinv = rec.rinv[a];
+        const float lof = (float)lo;  // the block minimum, an f32 value
         const uint32_t b = HAS_OFF ? (uint32_t)rec.b[a] : 0u;
         const uint32_t mks = ((1u << b) - 1u) << shift;
         float x[kSP];
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
           const double r = __dmul_rn(t, rinv);
           const uint32_t rl = (uint32_t)__double2loint(r);
           const uint32_t q = (uint32_t)__double2loint(__dadd_rz(r, 4503599627370496.0));
-          lowmin = min(lowmin, rl + 1u);
+          lowmin = min(lowmin, rl + (x[k] == lof ? 3u : 1u));  // x == lo: r == 0 is exact
           if (HAS_OFF) {
             seg[k] += (q >> b) * stride;
             off[k] |= (q << shift) & mks;
@@ -292,10 +295,10 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
       sm.uniq[r + 1] = (uint16_t)sg;
       if (HAS_OFF) {
         const uint32_t o = key[k] >> 16, sh = 4 * (o & 7);
-        const uint32_t old = atomicAdd(&sm.cnt[2 * r + (o >> 3)], 1u << sh);
+        const uint32_t old = atomicAdd(&sm.cnt[cnt_idx(r) | (o >> 3) << 10], 1u << sh);
         rk[k] = r | ((old >> sh) & 15u) << 10 | o << 14;
       } else {
-        atomicAdd(&sm.cnt[r], 1u);  // result unused: RED
+        atomicAdd(&sm.cnt[cnt_idx(r)], 1u);  // result unused: RED
         rk[k] = r;
       }
     }
@@ -309,16 +312,11 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
       const uint32_t u[9] = {u4.x & 0xffffu, u4.x >> 16, u4.y & 0xffffu, u4.y >> 16,
                              u4.z & 0xffffu, u4.z >> 16, u4.w & 0xffffu, u4.w >> 16, (uint32_t)sm.uniq[kSP * tid + kSP]};
       uint32_t cc[kSP];
-      if (HAS_OFF) {
 #pragma unroll
-        for (int j = 0; j < kSP; j += 2) {
-          const uint4 c2 = reinterpret_cast<const uint4*>(sm.cnt)[(kSP * tid + j) >> 1];
-          cc[j] = wide ? nib_sum8(c2.x) + nib_sum8(c2.y) : nib_sum1(c2.x);
-          cc[j + 1] = wide ? nib_sum8(c2.z) + nib_sum8(c2.w) : nib_sum1(c2.z);
-        }
-      } else {
-        const uint4 c0 = reinterpret_cast<const uint4*>(sm.cnt)[2 * tid], c1 = reinterpret_cast<const uint4*>(sm.cnt)[2 * tid + 1];
-        cc[0] = c0.x; cc[1] = c0.y; cc[2] = c0.z; cc[3] = c0.w; cc[4] = c1.x; cc[5] = c1.y; cc[6] = c1.z; cc[7] = c1.w;
+      for (int j = 0; j < kSP; ++j) {
+        const uint32_t cw = sm.cnt[(j << 7) | tid];
+        if (HAS_OFF) cc[j] = wide ? nib_sum8(cw) + nib_sum8(sm.cnt[1024 | (j << 7) | tid]) : nib_sum8(cw);
+        else cc[j] = cw;
       }
 #pragma unroll
       for (int j = 0; j < kSP; ++j) {
@@ -333,9 +331,9 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
     }
     // the bitmap becomes the payload stage: zero the words it used
     for (uint32_t g = tid; g < ng; g += kST) reinterpret_cast<uint4*>(sm.bm)[g] = z4;
-    if (!HAS_OFF && kSP * tid < (int)U) {  // counters are dead too (offset-free blocks)
-      reinterpret_cast<uint4*>(sm.cnt)[2 * tid] = z4;
-      reinterpret_cast<uint4*>(sm.cnt)[2 * tid + 1] = z4;
+    if (!HAS_OFF) {  // counters are dead too (offset-free blocks)
+#pragma unroll
+      for (int j = 0; j < kSP; ++j) sm.cnt[(j << 7) | tid] = 0u;
     }
     uint32_t total, ex;
     {
@@ -348,9 +346,10 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
     if (HAS_OFF && total != (uint32_t)kMaxBs) {
       // a nibble counter overflowed: the general CTA encoder takes this block
       // (block-uniform branch; nothing was written to the stage)
-      if (kSP * tid < (int)U) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) reinterpret_cast<uint4*>(sm.cnt)[4 * tid + i] = z4;
+      for (int j = 0; j < kSP; ++j) {
+        sm.cnt[(j << 7) | tid] = 0u;
+        sm.cnt[1024 | (j << 7) | tid] = 0u;
       }
       if (tid < 4) sm.orw[tid] = 0;
       if (tid == 0) {
@@ -360,6 +359,7 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
       __syncthreads();
       continue;
     }
+    const bool short_runs = sm.orw[0] < 16u;  // every run <= 15 particles
     const uint32_t w_cnt = bitlen32(sm.orw[0]), w_del = bitlen32(sm.orw[1]);
     const uint32_t w_off = HAS_OFF ? bitlen32(sm.orw[2]) : 0u;
     const uint32_t Ld = (U * w_del + 7) >> 3, Lc = (U * w_cnt + 7) >> 3;
@@ -425,10 +425,12 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
         const uint32_t m = (1u << (4 * (o & 7))) - 1u;
         uint32_t below;
         if (wide) {
-          const uint2 c = reinterpret_cast<const uint2*>(sm.cnt)[r];
-          below = o < 8 ? nib_sum8(c.x & m) : nib_sum8(c.x) + nib_sum8(c.y & m);
+          const uint32_t c0 = sm.cnt[cnt_idx(r)];
+          below = o < 8 ? nib_sum8(c0 & m) : nib_sum8(c0) + nib_sum8(sm.cnt[1024 | cnt_idx(r)] & m);
+        } else if (short_runs) {
+          below = nib_sum1(sm.cnt[cnt_idx(r)] & m);  // runs <= 15: one multiply
         } else {
-          below = nib_sum1(sm.cnt[2 * r] & m);
+          below = nib_sum8(sm.cnt[cnt_idx(r)] & m);
         }
         sm.u.o.soff[(uint32_t)sm.u.o.rstart[r] + below + ((rk[k] >> 10) & 15u)] = (uint8_t)o;
       }
@@ -444,9 +446,10 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
         or_bits32(st, bo + kSP * tid * w_off, v);
       }
       // counters and OR words are dead: zero them for the next block
-      if (kSP * tid < (int)U) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) reinterpret_cast<uint4*>(sm.cnt)[4 * tid + i] = z4;
+      for (int j = 0; j < kSP; ++j) {
+        sm.cnt[(j << 7) | tid] = 0u;
+        if (wide) sm.cnt[1024 | (j << 7) | tid] = 0u;
       }
       if (tid < 4) sm.orw[tid] = 0;
     }

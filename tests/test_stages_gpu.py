@@ -27,7 +27,7 @@ CONFIGS = [
     ("uniform", 2, np.float64, 1e-5, 512, 16),
     ("lattice", 1, np.float32, 1e-4, 256, 32),
     ("clusters", 3, np.float64, 1e-8, 1024, 64),  # 64-bit keys (1e-9 overflows, like the oracle)
-    ("uniform", 3, np.float32, 1e-8, 1024, 32),  # half-bound axes (the edge-snap quantizer)
+    ("uniform", 2, np.float32, 1e-8, 1024, 32),  # half-bound axes (the edge-snap quantizer); 3D overflows
 ]
 
 
