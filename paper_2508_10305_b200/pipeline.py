@@ -313,9 +313,18 @@ def compress_batch_device(datasets, cfg: CompressConfig, *, timing=None) -> list
         s.wait_event(start)
         with torch.cuda.stream(s):
             jobs.append(_compress_begin(ds, cfg, i, timing))
+    # the encoders run one dataset at a time (job i's waits for job i-1's):
+    # two compute-bound encoders sharing the SMs finish later than the two in
+    # sequence; only the HBM-bound range passes overlap an encoder
+    prev = None
     for i, j in enumerate(jobs):
-        with torch.cuda.stream(_side_stream(i)):
+        s = _side_stream(i)
+        if prev is not None:
+            s.wait_event(prev)
+        with torch.cuda.stream(s):
             _compress_encode(j)
+            prev = torch.cuda.Event()
+            prev.record(s)
     outs = []
     for i, j in enumerate(jobs):
         s = _side_stream(i)

@@ -268,9 +268,15 @@ def compress_batch_device(datasets, cfg: CompressConfig, *, timing=None) -> list
     for i, j in enumerate(jobs):
         with torch.cuda.stream(_side_stream(i)):
             _compress_plan(j)
+    prev = None  # one encoder at a time, as pipeline.compress_batch_device
     for i, j in enumerate(jobs):
-        with torch.cuda.stream(_side_stream(i)):
+        s = _side_stream(i)
+        if prev is not None:
+            s.wait_event(prev)
+        with torch.cuda.stream(s):
             _compress_encode(j)
+            prev = torch.cuda.Event()
+            prev.record(s)
     inf = 1 << 62
     rows, locals_ = [], []
     for i, j in enumerate(jobs):
