@@ -173,15 +173,9 @@ void launch_emit(const CompactParams& C, cudaStream_t s) {
 
 template <int D, bool F64>
 void launch_range(const EncParams& P, cudaStream_t s) {
-#ifdef GPZB_K1_CTA
-  const uint64_t grid = std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * 8);
-  GPZB_COUNT_LAUNCH();
-  k_range<D, typename std::conditional<F64, double, float>::type><<<(unsigned)grid, kThreads, 0, s>>>(P);
-#else
   const uint64_t grid = std::min<uint64_t>((P.nblocks + kWarps - 1) / kWarps, (uint64_t)sm_count() * GPZB_K1_CTAS);
   GPZB_COUNT_LAUNCH();
   k_range_w<D, typename std::conditional<F64, double, float>::type><<<(unsigned)grid, kThreads, 0, s>>>(P);
-#endif
 }
 
 template <int D, bool F64>

@@ -98,14 +98,6 @@ __device__ __forceinline__ int bitlen32(uint32_t v) { return v ? 32 - __clz((int
 __device__ __forceinline__ uint64_t mask64(unsigned bits) { return bits >= 64 ? ~0ull : ((1ull << bits) - 1); }
 
 // --------------------------------------------------- memory-order helpers
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 // Look-back status words carry their own payload (flag + value in one
 // 64-bit word), so relaxed gpu-scope accesses are sufficient.
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
@@ -145,12 +137,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
           smem_u32(bar)),
       "r"(parity)
       : "memory");
-}
-
-// Exact-division fallback of the certified quantizer, kept out of line so
-// the common path is a real branch rather than predicated division code.
-__device__ __noinline__ uint32_t exact_floor_div(double t, double w) {
-  return __double2uint_rz(__ddiv_rn(t, w));
 }
 
 // ------------------------------------------------------- block primitives

@@ -836,17 +836,6 @@ __device__ __forceinline__ void decode_general(const DecParams& P, DecSmem& sm, 
   }
 }
 
-template <int D, bool F64, bool PRES>
-__global__ void __launch_bounds__(kThreads, GPZB_K4_MINB) k_decode(const DecParams P) {
-  __shared__ DecSmem sm;
-  const uint64_t blk = blockIdx.x;
-  const DecRec* rec = P.rec + blk;
-  const uint32_t kind = rec->kind, fb = rec->fast_body;
-  if (kind != 0) return;
-  if (!PRES && fb) decode_fast<D, F64>(P, sm, blk, rec);
-  else decode_general<D, F64, PRES>(P, sm, blk, rec);
-}
-
 // Particle count of each block (iter_decompressed_blocks output offsets).
 __global__ void k_block_counts(const uint8_t* c, uint64_t len, uint64_t table_end, uint64_t payload_len,
                                uint64_t nblocks, uint64_t* counts) {

@@ -1,15 +1,15 @@
-// K1 (range) and K2 (fused encode) for the GPZ B200 compressor.
+// K1 (range) and K1.5 (geometry) of the GPZ B200 compressor, plus the
+// shared helpers of the encoders.
 //
-// Pipeline (all stream-ordered, one D2H of 8 bytes between K1.5 and K2):
-//   K1   k_range     per-block bounds, joint range (REL), finiteness
-//   K1.5 k_geometry  per-block geometry record; routes each block to the
-//                    32-bit fast encoder ("narrow") or the general one ("wide")
-//   K2w  k_encode_wide   general encoder (any width, preserve_order) into a
-//                        side buffer, only for the wide blocks
-//   K2   k_encode    narrow blocks: fused quantize -> bitmap counting sort ->
-//                    RLE/delta/width -> size -> decoupled look-back (overlapped
-//                    with bit-packing) -> realigned vector stores; wide blocks:
-//                    look-back + copy of the staged payload.
+// Compress pipeline (all stream-ordered; the host reads the 128-byte result
+// record once, after K3a, to size the exact container):
+//   K1   k_range_w       per-block bounds, joint range (REL), finiteness
+//   K1.5 k_geometry      per-block geometry record; routes each block to an
+//                        encoder (K2s / K2p / K2 / K2w lists, counts on the device)
+//   K2*  encoders        each block's payload into its staging slot, its
+//                        length into sizes[blk]
+//   K3a  k_scan_sizes    decoupled look-back scan of the lengths (gpzb_compact.cuh)
+//   K3b  k_copy_payloads table, global header, payloads to their final offsets
 #pragma once
 
 #include <type_traits>
@@ -75,133 +75,7 @@ __device__ __forceinline__ void load_particles(const EncParams& P, uint64_t firs
   }
 }
 
-// Per-axis min / max over the valid particles of the CTA's block
-// (quantizer.block_bounds, quantizer.py:51-57) + non-finite flags.
-// Result broadcast to every thread.  Contains one __syncthreads pair.
-template <int D, typename T>
-__device__ __forceinline__ void block_bounds(const T (&x)[D][kItems], int n, int p0, double (&lo)[D],
-                                             double (&hi)[D], uint32_t& nonfinite, void* ws_raw) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  nonfinite = 0;
-  if constexpr (sizeof(T) == 4) {
-    int* ws = reinterpret_cast<int*>(ws_raw);  // [D][2][kWarps]
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      int mn = 0x7fffffff, mx = (int)0x80000000;
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        if (p0 + k < n) {
-          float f = x[a][k];
-          if (!isfinite(f)) nonfinite |= 1u << a;
-          int key = fkey(f);
-          mn = min(mn, key);
-          mx = max(mx, key);
-        }
-      }
-      mn = __reduce_min_sync(kFull, mn);
-      mx = __reduce_max_sync(kFull, mx);
-      if (lane == 0) { ws[(a * 2) * kWarps + wid] = mn; ws[(a * 2 + 1) * kWarps + wid] = mx; }
-    }
-    nonfinite = __reduce_or_sync(kFull, nonfinite);
-    __syncthreads();
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      int mn = ws[(a * 2) * kWarps], mx = ws[(a * 2 + 1) * kWarps];
-#pragma unroll
-      for (int w = 1; w < kWarps; ++w) {
-        mn = min(mn, ws[(a * 2) * kWarps + w]);
-        mx = max(mx, ws[(a * 2 + 1) * kWarps + w]);
-      }
-      lo[a] = (double)fkey_inv(mn);
-      hi[a] = (double)fkey_inv(mx);
-    }
-    __syncthreads();
-  } else {
-    double* ws = reinterpret_cast<double*>(ws_raw);
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
-#pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        if (p0 + k < n) {
-          double f = (double)x[a][k];
-          if (!isfinite(f)) nonfinite |= 1u << a;
-          mn = fmin(mn, f);
-          mx = fmax(mx, f);
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        mn = fmin(mn, __shfl_xor_sync(kFull, mn, o));
-        mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
-      }
-      if (lane == 0) { ws[(a * 2) * kWarps + wid] = mn; ws[(a * 2 + 1) * kWarps + wid] = mx; }
-    }
-    nonfinite = __reduce_or_sync(kFull, nonfinite);
-    __syncthreads();
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      double mn = ws[(a * 2) * kWarps], mx = ws[(a * 2 + 1) * kWarps];
-#pragma unroll
-      for (int w = 1; w < kWarps; ++w) {
-        mn = fmin(mn, ws[(a * 2) * kWarps + w]);
-        mx = fmax(mx, ws[(a * 2 + 1) * kWarps + w]);
-      }
-      lo[a] = mn;
-      hi[a] = mx;
-    }
-    __syncthreads();
-  }
-  // nonfinite is warp-reduced only; callers OR it into the result record.
-}
-
 // ------------------------------------------------------------------- K1
-// Joint range of all axes (model.resolve_absolute_bound, model.py:194-195),
-// per-block bounds for K2, and the Dataset finiteness check (model.py:75-77).
-template <int D, typename T>
-__global__ void __launch_bounds__(kThreads) k_range(const EncParams P) {
-  __shared__ __align__(16) double ws[2][3 * 2 * kWarps];
-  const int p0 = threadIdx.x * kItems;
-  double run_lo = __longlong_as_double(0x7ff0000000000000ll), run_hi = -run_lo;
-  uint32_t nf_all = 0;
-  // two blocks per iteration: both loads are in flight before either reduction
-  for (uint64_t blk = blockIdx.x; blk < P.nblocks; blk += 2ull * gridDim.x) {
-    const uint64_t blk2 = blk + gridDim.x;
-    const bool has2 = blk2 < P.nblocks;
-    T x[2][D][kItems];
-    const uint64_t first = blk * (uint64_t)P.bs, first2 = blk2 * (uint64_t)P.bs;
-    const int n = (int)min((uint64_t)P.bs, P.count - first);
-    const int n2 = has2 ? (int)min((uint64_t)P.bs, P.count - first2) : 0;
-    load_particles<D, T>(P, first, n, p0, x[0]);
-    if (has2) load_particles<D, T>(P, first2, n2, p0, x[1]);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (h == 1 && !has2) break;
-      double lo[D], hi[D];
-      uint32_t nf;
-      block_bounds<D, T>(x[h], h ? n2 : n, p0, lo, hi, nf, ws[h]);
-      nf_all |= nf;
-      if (threadIdx.x == 0) {
-        T* out = reinterpret_cast<T*>(const_cast<void*>(P.bounds)) + (h ? blk2 : blk) * 2 * D;
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          out[2 * a] = (T)lo[a];
-          out[2 * a + 1] = (T)hi[a];
-          run_lo = fmin(run_lo, lo[a]);
-          run_hi = fmax(run_hi, hi[a]);
-        }
-      }
-    }
-  }
-  if (threadIdx.x == 0) {
-    if (run_lo <= run_hi) {
-      atomicMax(&P.res->range_w[0], ukey(-run_lo));
-      atomicMax(&P.res->range_w[1], ukey(run_hi));
-    }
-  }
-  if ((threadIdx.x & 31) == 0 && nf_all) atomicOr(&P.res->nonfinite_mask, nf_all);
-}
-
 // K1, warp per block: each warp streams whole blocks (16-byte loads, eight
 // per lane and axis in flight, no CTA barriers) and reduces them with warp
 // primitives; one atomic per CTA for the joint range.

@@ -48,10 +48,6 @@ struct NarrowSmem {
   __align__(16) U u;
 };
 
-__device__ __forceinline__ void named_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
 // Vectorised loads of a full block's 4 particles per thread (16-byte aligned axes).
 template <int D, typename T>
 __device__ __forceinline__ void load_full(const EncParams& P, uint64_t first, int p0, T (&x)[D][kItems]) {
