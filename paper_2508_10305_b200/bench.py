@@ -42,16 +42,24 @@ class GenKind(Enum):
 
 @dataclass(frozen=True)
 class GenSpec:
+    """One synthetic dataset (bench.py:20-50 field set).
+
+    The box is [0, extent)^dims.  ``clusters`` / ``sigma`` shape
+    GAUSSIAN_CLUSTERS (sigma in box units); ``pitch`` / ``jitter`` shape
+    JITTERED_LATTICE (grid spacing, and the uniform displacement bound per
+    axis).
+    """
+
     kind: GenKind
     count: int
     dims: int = 3
     seed: int = 0
     precision: Precision = Precision.F32
-    extent: float = 1.0  # box edge length, origin-anchored
+    extent: float = 1.0
     clusters: int = 32
-    sigma: float = 0.01  # cluster std dev, same units as extent
-    pitch: float = 0.05  # lattice spacing
-    jitter: float = 0.01  # max lattice displacement per axis
+    sigma: float = 0.01
+    pitch: float = 0.05
+    jitter: float = 0.01
 
     def __post_init__(self) -> None:
         if self.count <= 0:
@@ -137,23 +145,24 @@ class BenchRow:
     decomp_gbps: float
 
     def to_csv(self) -> str:
-        psnr = "inf" if math.isinf(self.psnr) else f"{self.psnr:.4f}"
-        return (
-            f"{self.spec.kind.value},{self.spec.count},{self.spec.dims},{self.spec.seed},"
-            f"{self.eb:g},{self.cr:.4f},{self.bitrate:.4f},{psnr},"
-            f"{self.comp_gbps:.4f},{self.decomp_gbps:.4f}"
-        )
+        """One line in BENCH_CSV_HEADER's column order (bench.py:108-116 formats)."""
+        four = lambda v: format(v, ".4f")  # noqa: E731
+        cols = [self.spec.kind.value, str(self.spec.count), str(self.spec.dims), str(self.spec.seed),
+                format(self.eb, "g"), four(self.cr), four(self.bitrate),
+                "inf" if math.isinf(self.psnr) else four(self.psnr),
+                four(self.comp_gbps), four(self.decomp_gbps)]
+        return ",".join(cols)
 
 
 def _timed(fn, repetitions: int):
-    """Median wall-clock seconds over repetitions; result from the last run (bench.py:119-127)."""
-    samples = []
-    result = None
+    """Call ``fn`` ``repetitions`` times; return (median seconds, the last
+    call's value) — the reference's timing rule (bench.py:119-127)."""
+    durations, out = [], None
     for _ in range(repetitions):
-        start = time.perf_counter()
-        result = fn()
-        samples.append(time.perf_counter() - start)
-    return statistics.median(samples), result
+        t0 = time.perf_counter()
+        out = fn()
+        durations.append(time.perf_counter() - t0)
+    return statistics.median(durations), out
 
 
 def run_bench(spec: GenSpec, eb_list, cfg: CompressConfig, repetitions: int = 3, workers: int = 1,
