@@ -7,8 +7,9 @@
 //
 // Per block (9 barriers with offsets, 7 without):
 //   quantize (certified reciprocal, quantizer.py:142-191) -> 32-bit key
-//        seg | off << 16 per particle; RED.OR into a presence bitmap over
-//        [0, Π N)                                                     | B1
+//        seg | off << 16 per particle                                  | Bz
+//        (the previous block's stage is out; the next block's bulk copy starts)
+//   RED.OR into a presence bitmap over [0, Π N)                        | B1
 //   word prefixes of the bitmap (up to four 16-byte groups per thread) | B2 B3
 //   segment rank r of each particle = prefix + popc below its bit; the
 //        rank's counter word gets 1 << 4*off (ATOMS: the returned nibble is
@@ -21,20 +22,18 @@
 //        (width_for, codec.py:107-112)                                | B5
 //   header + delta + count streams bit-packed into the shared stage
 //        (serialize_block / pack_fixed, container.py:102-121,
-//        codec.py:115-129)                                            | B6
+//        codec.py:115-129); run starts published                      | B6
 //   each particle's place in (seg, off) order = run start + particles of
 //        its run with a smaller offset (nibble sum below its nibble) + tie;
 //        its offset goes there                                        | B7
-//   the offset stream packed from the ordered offsets; bitmap and counters
-//        zeroed for the next block                                    | B8
-//   the stage to the block's staging slot (K3 concatenates), stage zeroed
-//        (it is the next block's bitmap)                              | B9
+//   the offset stream packed from the ordered offsets                 | B8
+//   the stage to the block's staging slot (K3 concatenates), zeroed behind
+//        the copy (it is the next block's bitmap)
 //
-// A (segment, offset) pair held by >= 16 particles overflows its nibble (or,
-// for Σ log2 m <= 3, a run of >= 16 particles defeats the one-multiply
-// nibble sum); either way the counts then sum to less than 1024 and the
-// block is handed to the general CTA encoder K2 (gpzb_encode_narrow.cuh)
-// through its list — exact in every case.
+// A (segment, offset) pair held by >= 16 particles overflows its nibble; the
+// counts then sum to less than 1024 and the block is handed to the general
+// CTA encoder K2 (gpzb_encode_narrow.cuh) through its list — exact in every
+// case.
 #pragma once
 
 #include "gpzb_encode_narrow.cuh"
@@ -54,6 +53,11 @@ constexpr uint32_t kSmallMaxPN = 65536;
 // payload <= 50 + 1024 * 16 / 8 + 1024 * 11 / 8 (no offsets) = 3,506 bytes
 // (with offsets: counts <= 8 bits, offsets <= 4 bits: 3,634 bytes)
 constexpr int kSmallStageWords = 1024;
+// Added to t * RN(1/w) by the quantizer's FMA: 2^-60 (1 + 5 * 2^-52), whose
+// low word (5) passes the certificate, so an exact zero (x == block minimum)
+// needs no special case; for r >= 2^-8 it moves the product by < 2^-8 ulp,
+// inside the certificate's two-ulp slack.
+constexpr unsigned long long kCertNudgeBits = 0x3C30000000000005ull;
 
 template <int D, bool HAS_OFF>
 struct SmallSmem {
@@ -67,20 +71,21 @@ struct SmallSmem {
   __align__(16) uint32_t orw[4];         // width ORs: counts, deltas, offsets
   // presence bitmap over segments (quantize .. ranks), then the payload stage
   __align__(16) uint32_t bm[kSmallMaxPN / 32];
-  union {
-    uint16_t wp[kSmallMaxPN / 32];       // set bits before each bitmap word (prefix .. ranks)
-    struct {
-      uint16_t rstart[kMaxBs];           // first sorted position of run r
-      uint8_t soff[kMaxBs];              // offsets in (seg, off) order
-    } o;
-  } u;
-  // per segment rank r: counter word(s), at cnt[h * 1024 + (r & 7) * 128 + (r >> 3)]
-  // (h = off >> 3) so that thread t's runs 8t..8t+7 are conflict-free
+  // set bits before each bitmap word (prefix .. ranks), then run starts
+  __align__(16) uint16_t wp[kSmallMaxPN / 32];
+  // per segment rank r: counter word cnt[r] (offsets 0-7, one nibble each)
+  // and cnt[1024 + r] (offsets 8-15); offset-free blocks: the run length
   __align__(16) uint32_t cnt[HAS_OFF ? 2 * kMaxBs : kMaxBs];
   __align__(16) uint16_t uniq[kMaxBs + 8];  // [0] = 0 sentinel, [r + 1] = unique id of rank r
 };
 static_assert(kSmallStageWords <= kSmallMaxPN / 32, "the stage reuses the bitmap");
-__device__ __forceinline__ uint32_t cnt_idx(uint32_t r) { return ((r & 7u) << 7) | (r >> 3); }
+
+// (1 << (w mod 32)) - 1 in one instruction (BMSK)
+__device__ __forceinline__ uint32_t bmsk_wrap(uint32_t w) {
+  uint32_t d;
+  asm("bmsk.wrap.b32 %0, 0, %1;" : "=r"(d) : "r"(w));
+  return d;
+}
 
 // Exclusive scan of one value per thread over the (kSW-warp) CTA with a
 // single barrier.  `ws` (16-byte aligned) is not rewritten before a later
@@ -104,9 +109,7 @@ __device__ __forceinline__ uint32_t small_excl_scan(uint32_t v, uint32_t& total,
 }
 
 // Sum of the nibbles of a counter word (each nibble <= 15).  Exact when the
-// sum is <= 15 (one multiply), the case of runs of <= 15 particles, which
-// Σ log2 m <= 3 blocks must have (a longer run reads short, and the
-// block-level count check hands the block back).
+// sum is <= 15 (one multiply): runs of <= 15 particles.
 __device__ __forceinline__ uint32_t nib_sum1(uint32_t x) { return (x * 0x11111111u) >> 28; }
 // Exact for any word (byte-wise fold first).
 __device__ __forceinline__ uint32_t nib_sum8(uint32_t x) {
@@ -120,18 +123,14 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 // One bulk copy of block `blk`'s coordinates and geometry record into shared
 // memory, completing on the CTA's mbarrier (one elected thread).
-template <int D>
-__device__ __forceinline__ void small_fetch(const EncParams& P, SmallSmem<D, true>* s0, SmallSmem<D, false>* s1,
-                                            uint32_t blk) {
-  float(*x)[kMaxBs] = s0 ? s0->x : s1->x;
-  BlkRec* r = s0 ? &s0->rec : &s1->rec;
-  unsigned long long* bar = s0 ? &s0->mbar : &s1->mbar;
-  mbar_expect_tx(reinterpret_cast<uint64_t*>(bar), D * kMaxBs * 4 + (uint32_t)sizeof(BlkRec));
+template <int D, bool HAS_OFF>
+__device__ __forceinline__ void small_fetch(const EncParams& P, SmallSmem<D, HAS_OFF>& s, uint32_t blk) {
+  mbar_expect_tx(reinterpret_cast<uint64_t*>(&s.mbar), D * kMaxBs * 4 + (uint32_t)sizeof(BlkRec));
 #pragma unroll
   for (int a = 0; a < D; ++a)
-    bulk_g2s(x[a], reinterpret_cast<const float*>(P.axes[a]) + (uint64_t)blk * kMaxBs, kMaxBs * 4,
-             reinterpret_cast<uint64_t*>(bar));
-  bulk_g2s(r, P.rec + blk, sizeof(BlkRec), reinterpret_cast<uint64_t*>(bar));
+    bulk_g2s(s.x[a], reinterpret_cast<const float*>(P.axes[a]) + (uint64_t)blk * kMaxBs, kMaxBs * 4,
+             reinterpret_cast<uint64_t*>(&s.mbar));
+  bulk_g2s(&s.rec, P.rec + blk, sizeof(BlkRec), reinterpret_cast<uint64_t*>(&s.mbar));
 }
 
 template <int D, bool HAS_OFF>
@@ -148,10 +147,6 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
   auto list_at = [&](uint32_t i) -> uint32_t {
     return HAS_OFF ? P.small_list[i] : P.small_list[P.nblocks - 1 - i];
   };
-  auto fetch = [&](uint32_t blk) {
-    if constexpr (HAS_OFF) small_fetch<D>(P, &sm, nullptr, blk);
-    else small_fetch<D>(P, nullptr, &sm, blk);
-  };
   const uint4 z4 = make_uint4(0, 0, 0, 0);
   // invariant at every block start: bitmap (= stage), counters and OR words are zero
   for (int i = tid; i < (int)(kSmallMaxPN / 128); i += kST) reinterpret_cast<uint4*>(sm.bm)[i] = z4;
@@ -162,35 +157,35 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
     mbar_init(reinterpret_cast<uint64_t*>(&sm.mbar), 1);
     mbar_fence_init();
     sm.blk = list_at(blockIdx.x);
-    fetch(sm.blk);
+    small_fetch<D, HAS_OFF>(P, sm, sm.blk);
   }
   __syncthreads();
 
   const uint32_t bm_s = smem_u32(sm.bm);
+  const double nudge = __longlong_as_double((long long)kCertNudgeBits);
   uint32_t phase = 0;
   for (uint32_t item = blockIdx.x; item < nlist; item += gridDim.x) {
     mbar_wait(reinterpret_cast<uint64_t*>(&sm.mbar), phase);
     phase ^= 1;
-    const uint64_t blk = sm.blk;
-    const BlkRec& rec = sm.rec;
-    // thread t: particles 4t..4t+3 and 512+4t..512+4t+3 of sm.x
-    auto xat = [&](int a, int k) -> float { return sm.x[a][(k < 4 ? 4 * tid : 4 * (kST + tid)) + (k & 3)]; };
-    const uint32_t PN = rec.PN;
-    const uint32_t sumb = HAS_OFF ? (uint32_t)rec.sumb : 0u;
+    // everything this block needs from the record, before the next bulk copy replaces it
+    const uint32_t blk = sm.blk;
+    const uint32_t PN = sm.rec.PN;
+    const uint32_t sumb = HAS_OFF ? (uint32_t)sm.rec.sumb : 0u;
+    const uint32_t w_hdr_b = HAS_OFF && lane < D ? (uint32_t)sm.rec.b[lane] : 0u;
+    const uint32_t w_hdr_n = lane < D ? sm.rec.N[lane] : 0u;
 
-    // ---- quantize -> key = seg | off << 16; presence bitmap over segments
+    // ---- quantize -> key = seg | off << 16
     uint32_t key[kSP], off_or = 0;
     {
       uint32_t seg[kSP], off[kSP];
 #pragma unroll
       for (int k = 0; k < kSP; ++k) { seg[k] = 0; off[k] = 0; }
-      uint32_t lowmin = ~0u;  // min over coordinates of (low word of r) + 1: <= 1 flags a possible failure
+      uint32_t mn = ~0u, mx = 0u;  // extremes of the low words: 0 or ~0 flags a possible failure
       uint32_t stride = 1, shift = 0;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        const double lo = rec.lo[a], rinv = rec.rinv[a];
-        const float lof = (float)lo;  // the block minimum, an f32 value
-        const uint32_t b = HAS_OFF ? (uint32_t)rec.b[a] : 0u;
+        const double lo = sm.rec.lo[a], rinv = sm.rec.rinv[a];
+        const uint32_t b = HAS_OFF ? (uint32_t)sm.rec.b[a] : 0u;
         const uint32_t mks = ((1u << b) - 1u) << shift;
         float x[kSP];
         {
@@ -202,12 +197,13 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
 #pragma unroll
         for (int k = 0; k < kSP; ++k) {
           // certified reciprocal quantizer (gpzb_common.cuh quantize_coord,
-          // mode 0); r == 0 (t == 0) is exact, its high word is zero
+          // mode 0) with the nudge: r > 0 always, t == 0 gives r = nudge
           const double t = __dsub_rn((double)x[k], lo);
-          const double r = __dmul_rn(t, rinv);
+          const double r = __fma_rn(t, rinv, nudge);
           const uint32_t rl = (uint32_t)__double2loint(r);
           const uint32_t q = (uint32_t)__double2loint(__dadd_rz(r, 4503599627370496.0));
-          lowmin = min(lowmin, rl + (x[k] == lof ? 3u : 1u));  // x == lo: r == 0 is exact
+          mn = min(mn, rl);
+          mx = max(mx, rl);
           if (HAS_OFF) {
             seg[k] += (q >> b) * stride;
             off[k] |= (q << shift) & mks;
@@ -215,30 +211,18 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
             seg[k] += q * stride;
           }
         }
-        stride *= rec.N[a];
+        stride *= sm.rec.N[a];
         shift += b;
       }
-      // rare: some low word is 0 or all ones.  Exact zeros (t == 0, the
-      // block minimum) pass the certificate; anything else is redone by
-      // exact division (identical wherever the certificate holds)
-      bool bad = false;
-      if (__any_sync(kFull, lowmin <= 1u) && lowmin <= 1u) {
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          const double lo = rec.lo[a], rinv = rec.rinv[a];
-#pragma unroll
-          for (int k = 0; k < kSP; ++k) {
-            const double r = __dmul_rn(__dsub_rn((double)xat(a, k), lo), rinv);
-            const uint32_t rl = (uint32_t)__double2loint(r), rh = (uint32_t)__double2hiint(r);
-            bad |= ((rl + 1u) <= 1u) & (rh != 0u);
-          }
-        }
-      }
+      // rare (a coordinate within an ulp of a bin edge): exact division for
+      // this thread's particles (identical wherever the certificate holds)
+      const bool bad = mn == 0u || mx == ~0u;
       if (__any_sync(kFull, bad) && bad) {
 #pragma unroll
         for (int k = 0; k < kSP; ++k) {
-          const uint64_t so = redo_exact<D, float>(xat(0, k), D > 1 ? xat(D > 1 ? 1 : 0, k) : 0.f,
-                                                   D > 2 ? xat(D > 2 ? 2 : 0, k) : 0.f, &rec);
+          auto xat = [&](int a) -> float { return sm.x[a][(k < 4 ? 4 * tid : 4 * (kST + tid)) + (k & 3)]; };
+          const uint64_t so = redo_exact<D, float>(xat(0), D > 1 ? xat(D > 1 ? 1 : 0) : 0.f,
+                                                   D > 2 ? xat(D > 2 ? 2 : 0) : 0.f, &sm.rec);
           seg[k] = (uint32_t)(so >> 32);
           off[k] = (uint32_t)so;
         }
@@ -247,18 +231,20 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
       for (int k = 0; k < kSP; ++k) {
         key[k] = seg[k] | (off[k] << 16);
         off_or |= off[k];
-        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(bm_s + ((seg[k] >> 3) & ~3u)), "r"(1u << (seg[k] & 31))
-                     : "memory");
       }
     }
-    const uint32_t w_hdr_b = HAS_OFF && lane < D ? (uint32_t)rec.b[lane] : 0u;  // header fields, read before
-    const uint32_t w_hdr_n = lane < D ? rec.N[lane] : 0u;                       // the record is overwritten
-    __syncthreads();  // B1: coordinates and record consumed
+    __syncthreads();  // Bz: coordinates and record consumed; the previous stage is out and zeroed
     if (tid == 0 && item + gridDim.x < nlist) {  // the next block's bulk copy overlaps this block's encode
       fence_proxy_async_smem();
       sm.blk = list_at(item + gridDim.x);
-      fetch(sm.blk);
+      small_fetch<D, HAS_OFF>(P, sm, sm.blk);
     }
+#pragma unroll
+    for (int k = 0; k < kSP; ++k) {
+      const uint32_t sg = key[k] & 0xffffu;
+      asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(bm_s + ((sg >> 3) & ~3u)), "r"(1u << (sg & 31)) : "memory");
+    }
+    __syncthreads();  // B1: presence bitmap complete
 
     // ---- bitmap word prefixes: thread t owns 16-byte groups [t*gpt, t*gpt + gpt)
     const uint32_t ng = (((PN + 31) >> 5) + 3) >> 2;  // <= 512
@@ -279,7 +265,7 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
         if (g < ng) {
           const uint4 q = reinterpret_cast<const uint4*>(sm.bm)[g];
           const uint32_t e1 = e + __popc(q.x), e2 = e1 + __popc(q.y), e3 = e2 + __popc(q.z);
-          reinterpret_cast<uint2*>(sm.u.wp)[g] = make_uint2(e | (e1 << 16), e2 | (e3 << 16));
+          reinterpret_cast<uint2*>(sm.wp)[g] = make_uint2(e | (e1 << 16), e2 | (e3 << 16));
           e = e3 + __popc(q.w);
         }
       }
@@ -291,14 +277,14 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
 #pragma unroll
     for (int k = 0; k < kSP; ++k) {
       const uint32_t sg = key[k] & 0xffffu, w = sg >> 5;
-      const uint32_t r = (uint32_t)sm.u.wp[w] + __popc(sm.bm[w] & ((1u << (sg & 31)) - 1u));
+      const uint32_t r = (uint32_t)sm.wp[w] + __popc(sm.bm[w] & bmsk_wrap(sg));
       sm.uniq[r + 1] = (uint16_t)sg;
       if (HAS_OFF) {
         const uint32_t o = key[k] >> 16, sh = 4 * (o & 7);
-        const uint32_t old = atomicAdd(&sm.cnt[cnt_idx(r) | (o >> 3) << 10], 1u << sh);
+        const uint32_t old = atomicAdd(&sm.cnt[r | (o >> 3) << 10], 1u << sh);
         rk[k] = r | ((old >> sh) & 15u) << 10 | o << 14;
       } else {
-        atomicAdd(&sm.cnt[cnt_idx(r)], 1u);  // result unused: RED
+        atomicAdd(&sm.cnt[r], 1u);  // result unused: RED
         rk[k] = r;
       }
     }
@@ -312,17 +298,31 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
       const uint32_t u[9] = {u4.x & 0xffffu, u4.x >> 16, u4.y & 0xffffu, u4.y >> 16,
                              u4.z & 0xffffu, u4.z >> 16, u4.w & 0xffffu, u4.w >> 16, (uint32_t)sm.uniq[kSP * tid + kSP]};
       uint32_t cc[kSP];
+      {
+        const uint4 a0 = reinterpret_cast<const uint4*>(sm.cnt)[2 * tid];
+        const uint4 a1 = reinterpret_cast<const uint4*>(sm.cnt)[2 * tid + 1];
+        const uint32_t cw[kSP] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        if (!HAS_OFF) {
 #pragma unroll
-      for (int j = 0; j < kSP; ++j) {
-        const uint32_t cw = sm.cnt[(j << 7) | tid];
-        if (HAS_OFF) cc[j] = wide ? nib_sum8(cw) + nib_sum8(sm.cnt[1024 | (j << 7) | tid]) : nib_sum8(cw);
-        else cc[j] = cw;
+          for (int j = 0; j < kSP; ++j) cc[j] = cw[j];
+          reinterpret_cast<uint4*>(sm.cnt)[2 * tid] = z4;  // counters are dead (offset-free blocks)
+          reinterpret_cast<uint4*>(sm.cnt)[2 * tid + 1] = z4;
+        } else if (wide) {
+          const uint4 b0 = reinterpret_cast<const uint4*>(sm.cnt)[256 + 2 * tid];
+          const uint4 b1 = reinterpret_cast<const uint4*>(sm.cnt)[256 + 2 * tid + 1];
+          const uint32_t cw2[kSP] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+          for (int j = 0; j < kSP; ++j) cc[j] = nib_sum8(cw[j]) + nib_sum8(cw2[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < kSP; ++j) cc[j] = nib_sum8(cw[j]);
+        }
       }
 #pragma unroll
       for (int j = 0; j < kSP; ++j) {
-        const bool in = (uint32_t)(kSP * tid + j) < U;
-        const uint32_t c = in ? cc[j] : 0u;
-        const uint32_t d = in ? u[j + 1] - u[j] : 0u;
+        // ranks >= U: the counter words are zero; their uniq entries are stale
+        const uint32_t c = cc[j];
+        const uint32_t d = (uint32_t)(kSP * tid + j) < U ? u[j + 1] - u[j] : 0u;
         csum += c;
         c_or |= c;
         d_or |= d;
@@ -331,10 +331,6 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
     }
     // the bitmap becomes the payload stage: zero the words it used
     for (uint32_t g = tid; g < ng; g += kST) reinterpret_cast<uint4*>(sm.bm)[g] = z4;
-    if (!HAS_OFF) {  // counters are dead too (offset-free blocks)
-#pragma unroll
-      for (int j = 0; j < kSP; ++j) sm.cnt[(j << 7) | tid] = 0u;
-    }
     uint32_t total, ex;
     {
       const uint32_t r0 = __reduce_or_sync(kFull, c_or), r1 = __reduce_or_sync(kFull, d_or);
@@ -346,17 +342,16 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
     if (HAS_OFF && total != (uint32_t)kMaxBs) {
       // a nibble counter overflowed: the general CTA encoder takes this block
       // (block-uniform branch; nothing was written to the stage)
-#pragma unroll
-      for (int j = 0; j < kSP; ++j) {
-        sm.cnt[(j << 7) | tid] = 0u;
-        sm.cnt[1024 | (j << 7) | tid] = 0u;
-      }
+      reinterpret_cast<uint4*>(sm.cnt)[2 * tid] = z4;
+      reinterpret_cast<uint4*>(sm.cnt)[2 * tid + 1] = z4;
+      reinterpret_cast<uint4*>(sm.cnt)[256 + 2 * tid] = z4;
+      reinterpret_cast<uint4*>(sm.cnt)[256 + 2 * tid + 1] = z4;
+      __syncthreads();  // every thread has read the OR words
       if (tid < 4) sm.orw[tid] = 0;
       if (tid == 0) {
         P.rec[blk].kind = KIND_NARROW;
         P.cta_list[atomicAdd(&R->cta_count, 1u)] = (uint32_t)blk;
       }
-      __syncthreads();
       continue;
     }
     const bool short_runs = sm.orw[0] < 16u;  // every run <= 15 particles
@@ -370,12 +365,12 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
       P.status[blk] = L;  // payload length for the K3 scan
       P.rec[blk].path = HAS_OFF ? 6 : 7;  // diagnostics: gpzb_encode_path_counts
     }
-    if (HAS_OFF && kSP * tid < (int)U) {  // run starts of runs 8t..8t+7 (one 16-byte store)
+    if (HAS_OFF && kSP * tid < (int)U) {  // run starts of runs 8t..8t+7 (one 16-byte store; wp is dead)
       uint32_t e[kSP];
       e[0] = ex;
 #pragma unroll
       for (int j = 1; j < kSP; ++j) e[j] = e[j - 1] + (dc[j - 1] >> 16);
-      reinterpret_cast<uint4*>(sm.u.o.rstart)[tid] =
+      reinterpret_cast<uint4*>(sm.wp)[tid] =
           make_uint4(e[0] | e[1] << 16, e[2] | e[3] << 16, e[4] | e[5] << 16, e[6] | e[7] << 16);
     }
     uint32_t* st = sm.bm;  // the payload stage
@@ -391,7 +386,7 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
         const uint32_t ab = 8 + a * 13;
         if (which < 2) {
           bpos = ab + which * 4;
-          val = __float_as_uint(reinterpret_cast<const float*>(P.bounds)[blk * 2 * D + 2 * a + which]);
+          val = __float_as_uint(reinterpret_cast<const float*>(P.bounds)[(uint64_t)blk * 2 * D + 2 * a + which]);
         } else if (which == 2) { bpos = ab + 8; val = hb; }
         else { bpos = ab + 9; val = hn; }
       } else if (f < 2 + 4 * D + 3) {
@@ -418,25 +413,26 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
     }
     if (HAS_OFF) {
       __syncthreads();  // B6: run starts visible
-      // ---- offsets into (seg, off) order
+      // ---- each particle's offset to its place in (seg, off) order
+      uint8_t* soff = reinterpret_cast<uint8_t*>(sm.wp + kMaxBs);
 #pragma unroll
       for (int k = 0; k < kSP; ++k) {
         const uint32_t r = rk[k] & 0x3ffu, o = rk[k] >> 14;
-        const uint32_t m = (1u << (4 * (o & 7))) - 1u;
+        const uint32_t m = bmsk_wrap(4 * o);  // nibbles below o's (o & 7)
         uint32_t below;
         if (wide) {
-          const uint32_t c0 = sm.cnt[cnt_idx(r)];
-          below = o < 8 ? nib_sum8(c0 & m) : nib_sum8(c0) + nib_sum8(sm.cnt[1024 | cnt_idx(r)] & m);
+          const uint32_t c0 = sm.cnt[r];
+          below = o < 8 ? nib_sum8(c0 & m) : nib_sum8(c0) + nib_sum8(sm.cnt[1024 | r] & m);
         } else if (short_runs) {
-          below = nib_sum1(sm.cnt[cnt_idx(r)] & m);  // runs <= 15: one multiply
+          below = nib_sum1(sm.cnt[r] & m);  // runs <= 15: one multiply
         } else {
-          below = nib_sum8(sm.cnt[cnt_idx(r)] & m);
+          below = nib_sum8(sm.cnt[r] & m);
         }
-        sm.u.o.soff[(uint32_t)sm.u.o.rstart[r] + below + ((rk[k] >> 10) & 15u)] = (uint8_t)o;
+        soff[(uint32_t)sm.wp[r] + below + ((rk[k] >> 10) & 15u)] = (uint8_t)o;
       }
       __syncthreads();  // B7
       if (w_off) {  // sorted offsets 8t..8t+7 (each < 16): one 32-bit window
-        const uint2 o8 = reinterpret_cast<const uint2*>(sm.u.o.soff)[tid];
+        const uint2 o8 = reinterpret_cast<const uint2*>(soff)[tid];
         uint32_t v = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -445,27 +441,28 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
         }
         or_bits32(st, bo + kSP * tid * w_off, v);
       }
-      // counters and OR words are dead: zero them for the next block
-#pragma unroll
-      for (int j = 0; j < kSP; ++j) {
-        sm.cnt[(j << 7) | tid] = 0u;
-        if (wide) sm.cnt[1024 | (j << 7) | tid] = 0u;
-      }
-      if (tid < 4) sm.orw[tid] = 0;
     }
-    __syncthreads();  // B8: the stage is complete
-    if (!HAS_OFF && tid < 4) sm.orw[tid] = 0;
+    __syncthreads();  // B8: the stage is complete; counters and OR words are dead
+    if (tid < 4) sm.orw[tid] = 0;
+    if (HAS_OFF) {  // zero this thread's counter words for the next block
+      reinterpret_cast<uint4*>(sm.cnt)[2 * tid] = z4;
+      reinterpret_cast<uint4*>(sm.cnt)[2 * tid + 1] = z4;
+      if (wide) {
+        reinterpret_cast<uint4*>(sm.cnt)[256 + 2 * tid] = z4;
+        reinterpret_cast<uint4*>(sm.cnt)[256 + 2 * tid + 1] = z4;
+      }
+    }
     // ---- the stage to this block's 16-byte aligned staging slot (K3 moves it
-    // into place); the stage words are zeroed behind the copy (bitmap invariant)
+    // into place); the stage words are zeroed behind the copy (bitmap invariant;
+    // the next block's Bz orders this before its bitmap)
     {
-      uint4* slot = reinterpret_cast<uint4*>(P.staging + blk * (uint64_t)kSlotBytes);
+      uint4* slot = reinterpret_cast<uint4*>(P.staging + (uint64_t)blk * kSlotBytes);
       const uint32_t nq = (L + 15) >> 4;
       for (uint32_t w = tid; w < nq; w += kST) {
         __stcg(slot + w, reinterpret_cast<const uint4*>(st)[w]);
         reinterpret_cast<uint4*>(st)[w] = z4;
       }
     }
-    __syncthreads();  // B9: the zeroed stage is the next block's bitmap
   }
 }
 
