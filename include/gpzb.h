@@ -212,6 +212,21 @@ int gpzb_quantize(const void* const* axes, int dims, int precision, uint64_t cou
                   uint32_t target_segs_per_axis, double eb_abs, const double* lohi, uint64_t* seg, uint64_t* off,
                   void* ws, uint64_t ws_bytes, void* stream, gpzb_result* res);
 
+/* pipeline._encode_block (pipeline.py:38-70) for every block with a given
+ * absolute bound (the value compress resolves, model.py:183-199): each
+ * block's serialised payload (serialize_block, container.py:98-121), back to
+ * back from `payloads`, and offsets[0..nblocks] (u64 device array,
+ * offsets[i] = where block i starts, offsets[nblocks] = the total) — the
+ * container without its global header.  payload_cap: gpzb_compress_bound
+ * minus 46 + 8 * (nblocks + 1) always suffices; when it is too small the
+ * call fails with GPZB_INVALID_ARGUMENT and res->out_len = the bytes needed.
+ * ws: gpzb_compress_workspace.  Synchronous; errors as compress (the first
+ * failing block). */
+int gpzb_encode_payloads(const void* const* axes, int dims, int precision, uint64_t count, uint32_t block_size,
+                         uint32_t target_segs_per_axis, int preserve_order, double eb_abs, uint8_t* payloads,
+                         uint64_t payload_cap, uint64_t* offsets, void* ws, uint64_t ws_bytes, void* stream,
+                         gpzb_result* res);
+
 /* container.compact's offsets (container.py:203-208): offsets[0] = 0,
  * offsets[i + 1] = offsets[i] + sizes[i] (u64, device arrays, nblocks + 1
  * outputs) by the K3a decoupled look-back scan.  Enqueued. */

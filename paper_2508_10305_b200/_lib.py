@@ -79,6 +79,8 @@ SIGNATURES = {
                                    _U64, _VP, _RES]),
     "gpzb_quantize": (_I32, [ctypes.POINTER(_VP), _I32, _I32, _U64, _U32, _U32, _D, _VP, _VP, _VP, _VP, _U64, _VP,
                              _RES]),
+    "gpzb_encode_payloads": (_I32, [ctypes.POINTER(_VP), _I32, _I32, _U64, _U32, _U32, _I32, _D, _VP, _U64, _VP,
+                                    _VP, _U64, _VP, _RES]),
     "gpzb_scan_workspace": (_I32, [_U64, ctypes.POINTER(_U64)]),
     "gpzb_scan_sizes": (_I32, [_VP, _U64, _VP, _VP, _U64, _VP]),
     "gpzb_parse_header": (_I32, [ctypes.c_char_p, _U64, _U64, _HDR, _RES]),

@@ -445,6 +445,65 @@ int gpzb_scan_sizes(const uint64_t* sizes, uint64_t nblocks, uint64_t* offsets, 
   return cuda_status(e);
 }
 
+int gpzb_encode_payloads(const void* const* axes, int dims, int prec, uint64_t count, uint32_t bs, uint32_t target,
+                         int pres, double eb_abs, uint8_t* payloads, uint64_t payload_cap, uint64_t* offsets, void* ws,
+                         uint64_t ws_bytes, void* stream, gpzb_result* res) {
+  clear_result(res);
+  int st = check_args(dims, prec, bs);
+  if (st) return res->status = st;
+  if (target == 0 || (target & (target - 1)) || !offsets) return res->status = GPZB_INVALID_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t nb = nblocks_of(count, bs);
+  if (nb == 0) {
+    cudaError_t e = cudaMemsetAsync(offsets, 0, 8, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return res->status = cuda_status(e);
+  }
+  // the compress sequence in ABS mode with the given bound (pipeline.py:38-70
+  // takes eb_abs directly), then K3b with the table pointed at `offsets` and
+  // no global header
+  void* side = nullptr;
+  uint64_t side_cap = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    st = gpzb_workspace_reset_async(ws, ws_bytes, count, bs, stream);
+    if (!st) st = gpzb_range_async(axes, dims, prec, count, bs, ws, ws_bytes, stream);
+    if (!st) st = gpzb_encode_plan_async(axes, dims, prec, count, eb_abs, GPZB_ABSOLUTE, bs, target, pres, ws, ws_bytes,
+                                         stream);
+    if (!st)
+      st = gpzb_encode_async(axes, dims, prec, count, eb_abs, GPZB_ABSOLUTE, bs, target, pres, ws, ws_bytes,
+                             static_cast<uint8_t*>(side), side_cap, nullptr, 0, 0, count, nb, 0, stream);
+    if (!st) st = gpzb_compress_result(ws, ws_bytes, count, bs, stream, res);
+    if (st != GPZB_NEED_SIDE || pass == 1) break;
+    side_cap = res->side_bytes;
+    cudaError_t e = cudaMallocAsync(&side, side_cap, s);
+    if (e != cudaSuccess) { st = cuda_status(e); side = nullptr; break; }
+  }
+  if (!st) {
+    const uint64_t total = res->out_len - GPZB_GLOBAL_HEADER_SIZE - 8 * (nb + 1);
+    res->out_len = total;
+    if (total > payload_cap || (total && !payloads)) {
+      st = GPZB_INVALID_ARGUMENT;  // res->out_len: the bytes needed
+    } else {
+      EncParams P = make_enc(axes, dims, prec, count, bs, ws);
+      P.side = static_cast<uint8_t*>(side);
+      CompactParams C = make_compact(P, dims, prec == GPZB_F64);
+      C.table0 = reinterpret_cast<uint8_t*>(offsets);
+      C.table = reinterpret_cast<uint8_t*>(offsets + 1);
+      C.table_base = 0;
+      C.header = nullptr;
+      C.payload = payloads;
+      launch_emit(C, s);
+      cudaError_t e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      st = cuda_status(e);
+    }
+  }
+  if (side) cudaFreeAsync(side, s);
+  if (st == GPZB_NEED_SIDE) st = GPZB_INVALID_ARGUMENT;
+  if (st && !res->status) res->status = st;
+  return st;
+}
+
 const char* gpzb_version(void) { return "gpzb 0.1 sm_100a"; }
 
 uint64_t gpzb_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }

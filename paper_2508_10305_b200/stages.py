@@ -5,6 +5,7 @@ these calls run one stage on its own:
 
 * ``block_geometry``  <- quantizer.block_bounds + derive_geometry (quantizer.py:51-129)
 * ``quantize``        <- quantizer.quantize_block, codes in input order (quantizer.py:223-247)
+* ``encode_payloads`` <- pipeline._encode_block for every block (pipeline.py:38-70)
 * ``scan_sizes``      <- container.compact's offsets (container.py:203-208)
 """
 
@@ -19,7 +20,7 @@ from ._lib import lib
 from .model import Dataset
 from .pipeline import _as_dataset, _check, _device_axes, _stream, _workspace
 
-__all__ = ["block_geometry", "quantize", "scan_sizes"]
+__all__ = ["block_geometry", "quantize", "encode_payloads", "scan_sizes"]
 
 
 def _prep(ds, block_size: int):
@@ -66,6 +67,29 @@ def quantize(ds: Dataset, eb_abs: float, block_size: int = 1024, target: int = 3
                            seg.data_ptr(), off.data_ptr(), ws.data_ptr(), ws.numel(), _stream(), ctypes.byref(res))
     _check(st, res)
     return seg[: ds.count], off[: ds.count]
+
+
+def encode_payloads(ds: Dataset, eb_abs: float, block_size: int = 1024, target: int = 32,
+                    preserve_order: bool = False):
+    """Every block's serialised payload (``_encode_block(slice, eb_abs, cfg,
+    prec)``) back to back, and the (B + 1) int64 offsets where each starts
+    (the last = the total), as CUDA tensors: the container minus its global
+    header."""
+    ds, axes, ws = _prep(ds, block_size)
+    nb = (ds.count + block_size - 1) // block_size
+    bound = ctypes.c_uint64()
+    _check(lib.gpzb_compress_bound(ds.count, ds.dims, ds.precision.value, block_size, target, int(preserve_order),
+                                   ctypes.byref(bound)))
+    cap = max(bound.value - 46 - 8 * (nb + 1), 1)
+    payloads = torch.empty(cap, dtype=torch.uint8, device=ws.device)
+    offsets = torch.empty(nb + 1, dtype=torch.int64, device=ws.device)
+    res = _lib.Result()
+    st = lib.gpzb_encode_payloads(_lib.ptr_array([a.data_ptr() for a in axes]), ds.dims, ds.precision.value,
+                                  ds.count, block_size, target, int(preserve_order), float(eb_abs),
+                                  payloads.data_ptr(), cap, offsets.data_ptr(), ws.data_ptr(), ws.numel(), _stream(),
+                                  ctypes.byref(res))
+    _check(st, res)
+    return payloads[: res.out_len].clone(), offsets
 
 
 def scan_sizes(sizes: torch.Tensor) -> torch.Tensor:

@@ -32,8 +32,18 @@ def _cuda():
     torch.cuda.set_device(0)
 
 
+@pytest.fixture(params=["default", "cta"])
+def route(request, monkeypatch):
+    """Encoder routing: the default (K2s / K2p for the blocks they take), or
+    GPZB_ROUTE=cta, which sends every narrow block to the general CTA
+    encoder K2 so that its sort paths stay pinned to the goldens too."""
+    if request.param == "cta":
+        monkeypatch.setenv("GPZB_ROUTE", "cta")
+    return request.param
+
+
 @pytest.mark.parametrize("name", case_ids())
-def test_golden_case(name):
+def test_golden_case(name, route):
     (_, gen, count, dims, dt, eb, mode, bs, t, pres, seed, extra) = case(name)
     want = GOLDEN["cases"][name]
     axes = make_axes(gen, count, dims, dt, seed, extra, O)
@@ -164,16 +174,25 @@ def test_nonfinite_abs_mode_detected_on_device():
         gz.compress(gz.Dataset.from_axes(axes), gz.CompressConfig(1e-3, eb_mode=gz.EbMode.ABSOLUTE))
 
 
-def test_sort_paths_are_all_exercised():
-    seen = np.zeros(8, np.int64)
-    for name in case_ids():
-        (_, gen, count, dims, dt, eb, mode, bs, t, pres, seed, extra) = case(name)
-        if GOLDEN["cases"][name]["error"] or count == 0:
-            continue
-        axes = make_axes(gen, count, dims, dt, seed, extra, O)
-        gz.compress_device(gz.Dataset.from_axes(axes), _cfg(eb, mode, bs, t, pres))
-        seen += np.array(gz.pipeline.last_path_counts())
-    assert (seen[:5] > 0).all(), seen
+def test_sort_paths_are_all_exercised(monkeypatch):
+    """Every offset-order path of K2 (GPZB_ROUTE=cta) and K2s (default
+    routing) runs on the golden cases (K2s's general-offset mode:
+    test_parity_extra_gpu.test_small_encoder_general_offsets)."""
+    seen = {"cta": np.zeros(8, np.int64), "default": np.zeros(8, np.int64)}
+    for route in ("cta", "default"):
+        if route == "cta":
+            monkeypatch.setenv("GPZB_ROUTE", "cta")
+        else:
+            monkeypatch.delenv("GPZB_ROUTE", raising=False)
+        for name in case_ids():
+            (_, gen, count, dims, dt, eb, mode, bs, t, pres, seed, extra) = case(name)
+            if GOLDEN["cases"][name]["error"] or count == 0:
+                continue
+            axes = make_axes(gen, count, dims, dt, seed, extra, O)
+            gz.compress_device(gz.Dataset.from_axes(axes), _cfg(eb, mode, bs, t, pres))
+            seen[route] += np.array(gz.pipeline.last_path_counts())
+    assert (seen["cta"][:5] > 0).all(), seen
+    assert seen["default"][6] > 0, seen
 
 
 def test_unsupported_block_size_is_loud():

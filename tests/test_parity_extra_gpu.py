@@ -182,3 +182,20 @@ def test_concurrent_threads_get_their_own_results():
     for t in th:
         t.join()
     assert not errs, errs
+
+
+@pytest.mark.parametrize("eb", [3e-3, 1e-3, 3e-4, 1e-4, 3e-5])
+def test_velocity_blocks_wide_offsets_ties_long_runs(eb):
+    """Velocity-like blocks from Σ log2 m <= 4 (K2s) to well above (K2's
+    offset-order paths), with repeated (segment, offset) pairs and a run of
+    200 identical particles: the whole container equals the oracle's."""
+    rng = np.random.default_rng(int(eb * 1e6))
+    n = 64 * 1024
+    bulk = np.repeat(rng.normal(0, 0.3, size=(64, 3)), 1024, axis=0)
+    pts = bulk + rng.normal(0, 0.05, size=(n, 3)) * rng.uniform(0.2, 3.0, size=(64, 1)).repeat(1024, axis=0)
+    pts[5 * 1024:5 * 1024 + 200] = pts[5 * 1024]            # one long run of identical particles
+    pts[9 * 1024:10 * 1024:2] = pts[9 * 1024 + 1:10 * 1024:2]  # pairs of identical particles
+    axes = [np.ascontiguousarray(pts[:, a]).astype(np.float32) for a in range(3)]
+    want = O.compress(axes, O.Config(eb))
+    got = gz.compress(gz.Dataset.from_axes(axes), gz.CompressConfig(error_bound=eb))
+    assert got == want

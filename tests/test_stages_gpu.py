@@ -63,6 +63,34 @@ def test_geometry_and_codes_match_oracle(cfg):
         assert np.array_equal(seg[sl], ws) and np.array_equal(off[sl], wo), b
 
 
+@pytest.mark.parametrize("cfg", CONFIGS, ids=lambda c: f"{c[0]}{c[1]}_{np.dtype(c[2]).name}_{c[3]}")
+@pytest.mark.parametrize("pres", [False, True])
+def test_encode_payloads_match_encode_block(cfg, pres):
+    """gpzb_encode_payloads: every block's payload equals the oracle's
+    _encode_block(slice, eb_abs, cfg, prec) (pipeline.py:38-70) byte for
+    byte, offsets included, at an absolute bound that is not the dataset's
+    own resolved one."""
+    kind, dims, dt, eb, bs, t = cfg
+    n = 20 * bs + bs // 3
+    axes = _axes(kind, dims, dt, n, 11)
+    prec = O.F64 if dt == np.float64 else O.F32
+    eb_abs = O.absolute_bound(axes, O.Config(eb)) * 1.37
+    ocfg = O.Config(eb, block_size=bs, target_segs_per_axis=t, preserve_order=pres)
+    try:
+        want = [O.encode_block([a[b * bs:(b + 1) * bs] for a in axes], eb_abs, ocfg, prec)
+                for b in range((n + bs - 1) // bs)]
+    except O.WidthOverflow:
+        with pytest.raises(gz.WidthOverflow):
+            stages.encode_payloads(gz.Dataset.from_axes(axes), eb_abs, bs, t, pres)
+        return
+    pay, offs = stages.encode_payloads(gz.Dataset.from_axes(axes), eb_abs, bs, t, pres)
+    offs = offs.cpu().numpy()
+    assert offs[0] == 0 and offs[-1] == pay.numel() == sum(len(w) for w in want)
+    got = bytes(pay.cpu().numpy())
+    for b, w in enumerate(want):
+        assert got[offs[b]:offs[b + 1]] == w, b
+
+
 def test_geometry_errors_match_oracle():
     # a block whose range over the bound needs more than 64-bit bin indices
     axes = [np.concatenate([np.zeros(1024), np.array([0.0, 1e300])]).astype(np.float64)]
