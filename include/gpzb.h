@@ -57,7 +57,7 @@ extern "C" {
 #define GPZB_RANGE_RELATIVE 1
 
 #define GPZB_GLOBAL_HEADER_SIZE 46   /* "<4sHBBBBddIQQ", container.py:57 */
-#define GPZB_MAX_BLOCK_SIZE 1024     /* kernels: one CTA of 256 threads x 4 particles per block */
+#define GPZB_MAX_BLOCK_SIZE (1u << 24) /* blocks above 1024 particles take K2b / K4b (workspace slices) */
 
 typedef struct gpzb_result {
   int32_t status;          /* GPZB_* class of the error the reference would raise first */

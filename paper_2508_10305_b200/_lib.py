@@ -15,7 +15,8 @@ LIB_PATH = os.environ.get("GPZB_LIB") or os.path.join(_HERE, "_gpzb.so")  # GPZB
 OK, DOMAIN, WIDTH, CORRUPT, UNSUPPORTED, INVALID, NEED_SIDE = 0, 1, 2, 3, 4, 5, 6
 F32, F64 = 0, 1
 GLOBAL_HEADER_SIZE = 46
-MAX_BLOCK_SIZE = 1024
+MAX_BLOCK_SIZE = 1 << 24   # K2b / K4b above 1024 particles per block (include/gpzb.h)
+CTA_BLOCK_SIZE = 1024      # the largest block one CTA holds (the fast kernels)
 
 
 class Result(ctypes.Structure):

@@ -11,6 +11,7 @@
 #include <mutex>
 #include <tuple>
 
+#include "gpzb_big.cuh"
 #include "gpzb_decode.cuh"
 #include "gpzb_decode_warp.cuh"
 #include "gpzb_encode.cuh"
@@ -37,12 +38,19 @@ std::atomic<unsigned long long> g_launches{0};
 inline uint64_t align_up(uint64_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
 
 struct EncLayout {
-  uint64_t status, tstat, bounds, rec, list, ctalist, slist, staging, total;
+  uint64_t status, tstat, bounds, rec, list, ctalist, slist, staging, big, total;
 };
+constexpr uint32_t kMaxBigBs = 1u << 24;  // K2b / K4b: larger blocks are refused (GPZB_UNSUPPORTED)
 
 inline uint64_t nblocks_of(uint64_t count, uint32_t bs) { return bs ? (count + bs - 1) / bs : 0; }
 
-EncLayout enc_layout(uint64_t nblocks, int dims, int prec) {
+int sm_count();
+// CTAs of K2b / K4b: one workspace slice each, at most ~1 GB of slices
+uint64_t big_grid(uint64_t nblocks, uint64_t slice) {
+  const uint64_t cap = std::max<uint64_t>(1, (1ull << 30) / slice);
+  return std::min<uint64_t>(std::min<uint64_t>(nblocks, (uint64_t)sm_count()), cap);
+}
+EncLayout enc_layout(uint64_t nblocks, int dims, int prec, uint32_t bs = kMaxBs) {
   EncLayout L;
   L.status = align_up(sizeof(DevResult));
   L.tstat = align_up(L.status + 8 * nblocks);
@@ -52,7 +60,9 @@ EncLayout enc_layout(uint64_t nblocks, int dims, int prec) {
   L.ctalist = align_up(L.list + 4 * nblocks);
   L.slist = align_up(L.ctalist + 4 * nblocks);
   L.staging = align_up(L.slist + 4 * nblocks);
-  L.total = align_up(L.staging + (uint64_t)kSlotBytes * nblocks);
+  // blocks of <= 1024 particles: one staging slot each; larger: K2b's slices
+  L.big = align_up(L.staging + (bs <= (uint32_t)kMaxBs ? (uint64_t)kSlotBytes * nblocks : 0));
+  L.total = align_up(L.big + (bs > (uint32_t)kMaxBs && nblocks ? big_grid(nblocks, big_enc_slice(bs)) * big_enc_slice(bs) : 0));
   return L;
 }
 
@@ -88,7 +98,7 @@ inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? GPZB_OK : GPZB
 int check_args(int dims, int prec, uint32_t bs) {
   if (dims < 1 || dims > 3 || (prec != GPZB_F32 && prec != GPZB_F64)) return GPZB_INVALID_ARGUMENT;
   if (bs == 0 || bs % 32) return GPZB_INVALID_ARGUMENT;
-  if (bs > (uint32_t)kMaxBs) return GPZB_UNSUPPORTED;
+  if (bs > kMaxBigBs) return GPZB_UNSUPPORTED;
   return GPZB_OK;
 }
 
@@ -187,6 +197,17 @@ void launch_geometry(const EncParams& P, cudaStream_t s) {
 
 template <int D, bool F64>
 void launch_encode(const EncParams& P, cudaStream_t s) {
+  if (P.bs > (uint32_t)kMaxBs) {  // K2b: every block of the call is on the general list
+    const unsigned grid = (unsigned)big_grid(P.nblocks, big_enc_slice(P.bs));
+    GPZB_COUNT_LAUNCH();
+    if (P.preserve) k_encode_big<D, F64, true><<<grid, kThreads, 0, s>>>(P, P.big);
+    else k_encode_big<D, F64, false><<<grid, kThreads, 0, s>>>(P, P.big);
+    GPZB_COUNT_LAUNCH();
+    const CompactParams C = make_compact(P, D, F64);
+    k_scan_sizes<<<(unsigned)((P.nblocks + kScanTile - 1) / kScanTile), kScanThreads, 0, s>>>(C);
+    if (P.payload) launch_emit(C, s);
+    return;
+  }
   {  // K2w: persistent over K1.5's list of general blocks (usually empty)
     const unsigned grid = (unsigned)std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * 4);
     if (P.preserve) { GPZB_COUNT_LAUNCH(); k_encode_wide<D, F64, true><<<grid, kThreads, 0, s>>>(P); }
@@ -225,6 +246,19 @@ void launch_decode(const DecParams& P, bool pres, cudaStream_t s) {
   const uint64_t nb = P.blk_hi - P.blk_lo;
   const unsigned pgrid = (unsigned)((nb + 255) / 256);
   const unsigned lgrid = (unsigned)std::min<uint64_t>(nb, (uint64_t)sm_count() * GPZB_K4_MINB);
+  if (P.bs > (uint32_t)kMaxBs) {  // K4a lists every block for K4b
+    const unsigned grid = (unsigned)big_grid(nb, big_dec_slice(P.bs));
+    GPZB_COUNT_LAUNCH();
+    GPZB_COUNT_LAUNCH();
+    if (pres) {
+      k_decode_plan<D, F64, true><<<pgrid, 256, 0, s>>>(P);
+      k_decode_big<D, F64, true><<<grid, kThreads, 0, s>>>(P, P.big);
+    } else {
+      k_decode_plan<D, F64, false><<<pgrid, 256, 0, s>>>(P);
+      k_decode_big<D, F64, false><<<grid, kThreads, 0, s>>>(P, P.big);
+    }
+    return;
+  }
   if (pres) {
     GPZB_COUNT_LAUNCH();
     k_decode_plan<D, F64, true><<<pgrid, 256, 0, s>>>(P);
@@ -294,7 +328,7 @@ EncParams make_enc(const void* const* axes, int dims, int prec, uint64_t count, 
   EncParams P;
   memset(&P, 0, sizeof(P));
   const uint64_t nb = nblocks_of(count, bs);
-  const EncLayout L = enc_layout(nb, dims, prec);
+  const EncLayout L = enc_layout(nb, dims, prec, bs);
   bool vec = true;
   for (int a = 0; a < dims; ++a) {
     P.axes[a] = axes[a];
@@ -313,6 +347,7 @@ EncParams make_enc(const void* const* axes, int dims, int prec, uint64_t count, 
   P.wide_list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + L.list);
   P.cta_list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + L.ctalist);
   P.small_list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + L.slist);
+  P.big = static_cast<uint8_t*>(ws) + L.big;
   // routing switches (diagnostics / A-B runs): GPZB_ROUTE=cta sends every
   // narrow block to the general CTA encoder K2, GPZB_ROUTE=small0 sends the
   // offset-free full f32 blocks to K2s instead of the warp encoder K2p
@@ -375,7 +410,7 @@ int gpzb_block_geometry(const void* const* axes, int dims, int prec, uint64_t co
   if (st) return res->status = st;
   if (target == 0 || (target & (target - 1))) return res->status = GPZB_INVALID_ARGUMENT;
   const uint64_t nb = nblocks_of(count, bs);
-  const EncLayout L = enc_layout(nb, dims, prec);
+  const EncLayout L = enc_layout(nb, dims, prec, bs);
   if (ws_bytes < L.total) return res->status = GPZB_INVALID_ARGUMENT;
   if (nb == 0) return GPZB_OK;
   cudaStream_t s = (cudaStream_t)stream;
@@ -397,7 +432,7 @@ int gpzb_quantize(const void* const* axes, int dims, int prec, uint64_t count, u
   if (st) return res->status = st;
   if (target == 0 || (target & (target - 1))) return res->status = GPZB_INVALID_ARGUMENT;
   const uint64_t nb = nblocks_of(count, bs);
-  const EncLayout L = enc_layout(nb, dims, prec);
+  const EncLayout L = enc_layout(nb, dims, prec, bs);
   if (ws_bytes < L.total) return res->status = GPZB_INVALID_ARGUMENT;
   if (nb == 0) return GPZB_OK;
   static_assert(3 * sizeof(AxisGeo) <= kSlotBytes, "geometry records fit the staging slots");
@@ -552,7 +587,7 @@ const char* gpzb_reason_message(int r) {
     case R_BLK_WINDOW: return "block payload exceeds the CUDA decoder's 24 KB window (oversized stream widths)";
     case R_NONFINITE_OUT: return "contains non-finite coordinates";
     case R_TOTAL: return "blocks decode to a different particle count than the header";
-    case R_UNSUPPORTED_BS: return "block_size above the CUDA kernels' 1024-particle limit";
+    case R_UNSUPPORTED_BS: return "block_size above the CUDA kernels' limit (2^24 particles)";
     default: return "unknown";
   }
 }
@@ -576,12 +611,20 @@ int gpzb_compress_bound(uint64_t count, int dims, int prec, uint32_t bs, uint32_
 int gpzb_compress_workspace(uint64_t count, int dims, int prec, uint32_t bs, uint64_t* ws_bytes) {
   int st = check_args(dims, prec, bs);
   if (st) return st;
-  *ws_bytes = enc_layout(nblocks_of(count, bs), dims, prec).total;
+  *ws_bytes = enc_layout(nblocks_of(count, bs), dims, prec, bs).total;
   return GPZB_OK;
 }
 
+// Decompress workspace: result record, one DecRec per block, K4a's list and,
+// for blocks of more than 1024 particles, K4b's slices.
+uint64_t dec_big_bytes(const gpzb_header* h) {
+  if (h->block_size <= (uint32_t)kMaxBs || h->block_count == 0) return 0;
+  return big_grid(h->block_count, big_dec_slice(h->block_size)) * big_dec_slice(h->block_size);
+}
+
 int gpzb_decompress_workspace(const gpzb_header* h, uint64_t* ws_bytes) {
-  *ws_bytes = align_up(sizeof(DevResult)) + align_up(h->block_count * sizeof(DecRec)) + align_up(4 * h->block_count);
+  *ws_bytes = align_up(sizeof(DevResult)) + align_up(h->block_count * sizeof(DecRec)) + align_up(4 * h->block_count) +
+              dec_big_bytes(h);
   return GPZB_OK;
 }
 
@@ -604,7 +647,7 @@ int gpzb_range_async(const void* const* axes, int dims, int prec, uint64_t count
   int st = check_args(dims, prec, bs);
   if (st) return st;
   const uint64_t nb = nblocks_of(count, bs);
-  if (ws_bytes < enc_layout(nb, dims, prec).total) return GPZB_INVALID_ARGUMENT;
+  if (ws_bytes < enc_layout(nb, dims, prec, bs).total) return GPZB_INVALID_ARGUMENT;
   if (nb == 0) return GPZB_OK;
   EncParams P = make_enc(axes, dims, prec, count, bs, ws);
   DISPATCH_DP(dims, prec, launch_range, P, (cudaStream_t)stream);
@@ -617,7 +660,7 @@ int gpzb_encode_plan_async(const void* const* axes, int dims, int prec, uint64_t
   if (st) return st;
   if (target == 0 || (target & (target - 1))) return GPZB_INVALID_ARGUMENT;
   const uint64_t nb = nblocks_of(count, bs);
-  if (ws_bytes < enc_layout(nb, dims, prec).total) return GPZB_INVALID_ARGUMENT;
+  if (ws_bytes < enc_layout(nb, dims, prec, bs).total) return GPZB_INVALID_ARGUMENT;
   if (nb == 0) return GPZB_OK;
   EncParams P = make_enc(axes, dims, prec, count, bs, ws);
   P.target = target;
@@ -636,7 +679,7 @@ int gpzb_encode_async(const void* const* axes, int dims, int prec, uint64_t coun
   if (st) return st;
   if (target == 0 || (target & (target - 1))) return GPZB_INVALID_ARGUMENT;
   const uint64_t nb = nblocks_of(count, bs);
-  if (ws_bytes < enc_layout(nb, dims, prec).total) return GPZB_INVALID_ARGUMENT;
+  if (ws_bytes < enc_layout(nb, dims, prec, bs).total) return GPZB_INVALID_ARGUMENT;
   uint64_t bound = 0;
   gpzb_compress_bound(count, dims, prec, bs, target, pres, &bound);
   if (out && out_cap < bound) return GPZB_INVALID_ARGUMENT;
@@ -661,7 +704,7 @@ int gpzb_emit_async(const void* const* axes, int dims, int prec, uint64_t count,
   int st = check_args(dims, prec, bs);
   if (st) return st;
   const uint64_t nb = nblocks_of(count, bs);
-  if (ws_bytes < enc_layout(nb, dims, prec).total) return GPZB_INVALID_ARGUMENT;
+  if (ws_bytes < enc_layout(nb, dims, prec, bs).total) return GPZB_INVALID_ARGUMENT;
   if (!out || out_cap < GPZB_GLOBAL_HEADER_SIZE + 8 * (nb + 1)) return GPZB_INVALID_ARGUMENT;
   if (nb == 0) return GPZB_OK;
   EncParams P = make_enc(axes, dims, prec, count, bs, ws);
@@ -709,7 +752,7 @@ int gpzb_encode_path_counts(void* ws, uint64_t ws_bytes, uint64_t count, uint32_
                             void* stream, uint64_t* counts) {
   if (check_args(dims, prec, bs)) return GPZB_INVALID_ARGUMENT;
   const uint64_t nb = nblocks_of(count, bs);
-  const EncLayout L = enc_layout(nb, dims, prec);
+  const EncLayout L = enc_layout(nb, dims, prec, bs);
   if (ws_bytes < L.total) return GPZB_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
   unsigned long long* dev = &reinterpret_cast<DevResult*>(ws)->path_blocks[0];
@@ -813,7 +856,7 @@ int gpzb_block_counts_async(const uint8_t* c, uint64_t len, const gpzb_header* h
   if (h->block_count == 0) return GPZB_OK;
   const unsigned grid = (unsigned)((h->block_count + 255) / 256);
   GPZB_COUNT_LAUNCH();
-  k_block_counts<<<grid, 256, 0, (cudaStream_t)stream>>>(c, len, h->table_end, h->payload_len, h->block_count,
+  k_block_counts<<<grid, 256, 0, (cudaStream_t)stream>>>(c, len, h->table_end, h->payload_len, h->block_count, h->block_size,
                                                           counts);
   return cuda_status(cudaGetLastError());
 }
@@ -849,6 +892,8 @@ int gpzb_decompress_range_async(const uint8_t* c, uint64_t len, const gpzb_heade
   if (ws_bytes < list_off + 4 * h->block_count) return GPZB_INVALID_ARGUMENT;
   P.rec = reinterpret_cast<DecRec*>(static_cast<uint8_t*>(ws) + align_up(sizeof(DevResult)));
   P.list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + list_off);
+  P.big = static_cast<uint8_t*>(ws) + list_off + align_up(4 * h->block_count);
+  if (ws_bytes < list_off + align_up(4 * h->block_count) + dec_big_bytes(h)) return GPZB_INVALID_ARGUMENT;
   P.blk_lo = first_block;
   P.blk_hi = last_block;
   DISPATCH_DP(h->dims, h->precision, launch_decode, P, h->preserve_order != 0, s);
@@ -937,6 +982,7 @@ int gpzb_pair_blocks(const void* const* orig, const void* const* rec, int dims, 
                      int64_t* rec_idx, void* ws, uint64_t ws_bytes, void* stream, gpzb_result* res) {
   clear_result(res);
   int st = check_args(dims, prec, bs);
+  if (!st && bs > (uint32_t)kMaxBs) st = GPZB_UNSUPPORTED;  // K5a: one CTA holds a whole block
   if (st) return res->status = st;
   if ((rprec != GPZB_F32 && rprec != GPZB_F64) || target == 0 || (target & (target - 1)))
     return res->status = GPZB_INVALID_ARGUMENT;

@@ -16,7 +16,7 @@ namespace gpzb {
 constexpr int kThreads = 256;             // CTA size of every block-level kernel
 constexpr int kWarps = kThreads / 32;
 constexpr int kItems = 4;                 // particles per thread
-constexpr int kMaxBs = kThreads * kItems; // GPZB_MAX_BLOCK_SIZE
+constexpr int kMaxBs = kThreads * kItems; // the block one CTA holds (larger ones: gpzb_big.cuh)
 constexpr unsigned kFull = 0xffffffffu;
 
 // ---------------------------------------------------------------- reasons

@@ -65,6 +65,7 @@ struct DecParams {
   DecRec* rec;
   uint32_t* list;          // K4a: blocks for the CTA decoder (count in res->wide_count)
   uint64_t blk_lo, blk_hi; // this launch decodes blocks [blk_lo, blk_hi) (chunked host pipelines)
+  uint8_t* big;            // K4b: per-CTA workspace slices (block_size > 1024)
 };
 
 constexpr int kDecStageWords = 5120;  // 20 KB payload window (legit blocks <= 19.2 KB)
@@ -159,8 +160,12 @@ __global__ void __launch_bounds__(256) k_decode_plan(const DecParams P) {
     }
     const __int128 want = (blk + 1 < P.nblocks) ? (__int128)P.bs
                           : (__int128)P.count - (__int128)P.bs * (__int128)(P.nblocks - 1);
-    if (!e && L > (uint64_t)(kDecStageWords * 4 - 16)) e = R_BLK_WINDOW;  // only with oversized widths
-    if (!e && n > (uint32_t)kMaxBs) e = ((__int128)n == want) ? R_UNSUPPORTED_BS : R_BLK_TOO_BIG;
+    if (P.bs <= (uint32_t)kMaxBs) {  // CTA decoders: the payload window and 1024 particles
+      if (!e && L > (uint64_t)(kDecStageWords * 4 - 16)) e = R_BLK_WINDOW;  // only with oversized widths
+      if (!e && n > (uint32_t)kMaxBs) e = ((__int128)n == want) ? R_UNSUPPORTED_BS : R_BLK_TOO_BIG;
+    } else if (!e && n > P.bs) {  // K4b: per-CTA slices of block_size particles
+      e = R_BLK_TOO_BIG;
+    }
     // per-block count vs the boundary math (pipeline.py:174-181), ranked
     // behind every decode check of the same block by the host
     if (!e && (__int128)n != want) atomicMax(&R->err_count, err_code(blk, 0, R_BLK_COUNT));
@@ -222,7 +227,7 @@ __global__ void __launch_bounds__(256) k_decode_plan(const DecParams P) {
   rec.pn_all = pn >= ((unsigned __int128)1 << 64);
   rec.pn_big = pn > 0xffffffffull;
   rec.sumb = (uint8_t)sumb;
-  rec.fast_body = (n == (uint32_t)kMaxBs && !PRES && w4[0] <= 32 && w4[1] <= 32 && w4[2] <= 32 && sumb <= 32 &&
+  rec.fast_body = (n == (uint32_t)kMaxBs && P.bs <= (uint32_t)kMaxBs && !PRES && w4[0] <= 32 && w4[1] <= 32 && w4[2] <= 32 && sumb <= 32 &&
                    !rec.pn_big && rec.fast_mask == (1u << D) - 1 && rec.chk_mask == 0 && rec.geo_bits == 0)
                       ? 1 : 0;
   if (rec.fast_body) {
@@ -838,14 +843,14 @@ __device__ __forceinline__ void decode_general(const DecParams& P, DecSmem& sm, 
 
 // Particle count of each block (iter_decompressed_blocks output offsets).
 __global__ void k_block_counts(const uint8_t* c, uint64_t len, uint64_t table_end, uint64_t payload_len,
-                               uint64_t nblocks, uint64_t* counts) {
+                               uint64_t nblocks, uint32_t bs, uint64_t* counts) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= nblocks) return;
   const uint8_t* table = c + GPZB_GLOBAL_HEADER_SIZE;
   const uint64_t e0 = ld_le(table + 8 * i, 8), e1 = ld_le(table + 8 * i + 8, 8);
   uint64_t n = 0;
   if (e0 + 4 <= e1 && e1 <= payload_len) n = ld_le(c + table_end + e0, 4);
-  counts[i] = min(n, (uint64_t)kMaxBs);
+  counts[i] = min(n, (uint64_t)max(bs, (uint32_t)kMaxBs));
 }
 
 }  // namespace gpzb

@@ -45,6 +45,7 @@ struct EncParams {
   uint32_t* wide_list;     // blocks routed to the general encoder
   uint32_t* cta_list;      // narrow blocks for the general CTA encoder K2 (K1.5, then K2s hand-backs)
   uint32_t* small_list;    // K2s blocks: with offsets from the front, offset-free from the back
+  uint8_t* big;            // K2b: per-CTA workspace slices (block_size > 1024)
   int small0;              // route offset-free full f32 blocks to K2s (1) or to the warp encoder K2p (0)
   int use_small;           // route blocks to K2s at all (diagnostics switch)
   uint8_t* side;           // staging for the general encoder's payloads
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(256) k_geometry(const EncParams P) {
   }
   unsigned __int128 PN = 1;
   uint32_t sumb = 0;
-  bool narrow = !P.preserve;
+  bool narrow = !P.preserve && P.bs <= (uint32_t)kMaxBs;  // larger blocks: K2b, through the general list
   if (!err) {
 #pragma unroll
     for (int a = 0; a < D; ++a) {

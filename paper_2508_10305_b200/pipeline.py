@@ -711,7 +711,7 @@ def resolve_absolute_bound(ds: Dataset, cfg: CompressConfig) -> float:
     if ds.count == 0:
         raise DomainError("range-relative bound is undefined for an empty dataset")
     axes = _device_axes(ds)
-    bs = min(cfg.block_size, _lib.MAX_BLOCK_SIZE)
+    bs = min(cfg.block_size, _lib.CTA_BLOCK_SIZE)  # the joint range does not depend on the block size
     ws_bytes = ctypes.c_uint64()
     _check(lib.gpzb_compress_workspace(ds.count, ds.dims, ds.precision.value, bs, ctypes.byref(ws_bytes)))
     ws = _workspace(ws_bytes.value)

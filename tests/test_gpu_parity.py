@@ -196,8 +196,66 @@ def test_sort_paths_are_all_exercised(monkeypatch):
 
 
 def test_unsupported_block_size_is_loud():
+    """Above 2^24 particles per block the library refuses (the workspace
+    slices of K2b / K4b would not fit); the reference has no limit."""
     with pytest.raises(NotImplementedError):
-        gz.compress(gz.Dataset.from_axes([np.zeros(4096, np.float32)]), gz.CompressConfig(1e-3, block_size=2048))
+        gz.compress(gz.Dataset.from_axes([np.zeros(64, np.float32)]), gz.CompressConfig(1e-3, block_size=1 << 25))
+
+
+BIG_CASES = [  # (kind, dims, dtype, eb, mode, block_size, target, preserve_order, n)
+    ("clusters", 3, np.float32, 1e-3, 1, 2048, 32, False, 5 * 2048 + 77),
+    ("clusters", 3, np.float32, 1e-4, 1, 4096, 32, True, 3 * 4096 + 1),
+    ("uniform", 2, np.float64, 1e-5, 1, 1056, 16, False, 4 * 1056 + 1055),
+    ("lattice", 1, np.float32, 1e-4, 0, 8192, 64, True, 2 * 8192 + 5),
+    ("uniform", 3, np.float32, 1e-7, 1, 2048, 32, False, 2048 + 3),  # half-bound axes / wide keys
+    ("clusters", 2, np.float64, 1e-9, 1, 65536, 32, False, 65536 + 999),
+]
+
+
+@pytest.mark.parametrize("case_", BIG_CASES, ids=lambda c: f"{c[0]}{c[1]}_{np.dtype(c[2]).name}_bs{c[5]}")
+def test_block_size_above_1024(case_):
+    """block_size > 1024 (any positive multiple of 32, model.py:118-119):
+    K2b / K4b give the oracle's container, errors and reconstruction, also
+    through iter_decompressed_blocks and the chunked host decode."""
+    kind, dims, dt, eb, mode, bs, t, pres, n = case_
+    gen = {"clusters": O.gen_clusters, "uniform": O.gen_uniform, "lattice": O.gen_lattice}[kind]
+    axes = gen(n, dims=dims, seed=bs + n, prec=O.F64 if dt == np.float64 else O.F32)
+    ocfg = O.Config(eb, mode, bs, t, pres)
+    try:
+        want, werr = O.compress(axes, ocfg), None
+    except O.OracleError as exc:
+        want, werr = None, (type(exc).__name__, error_prefix(str(exc)))
+    got, gerr = _outcome(lambda: gz.compress(gz.Dataset.from_axes(axes), _cfg(eb, mode, bs, t, pres)))
+    assert gerr == werr
+    if werr:
+        return
+    assert got == want
+    rec = gz.decompress(got)
+    for x, y in zip(rec.axes, O.decompress(want)):
+        assert np.array_equal(x, y)
+    blocks = list(gz.iter_decompressed_blocks(got))
+    assert len(blocks) == (n + bs - 1) // bs
+    for a in range(dims):
+        assert np.array_equal(np.concatenate([b[a] for b in blocks]), rec.axes[a])
+
+
+def test_block_size_above_1024_corruption():
+    """Bit flips in a container of 2048-particle blocks: the error class and
+    block of the oracle's decoder (pipeline.py:160-205), flip by flip."""
+    axes = O.gen_clusters(3 * 2048 + 100, dims=3, seed=9)
+    blob = O.compress(axes, O.Config(1e-3, block_size=2048))
+    rng = np.random.default_rng(5)
+    for bit in rng.choice(len(blob) * 8, size=300, replace=False):
+        bad = bytearray(blob)
+        bad[bit // 8] ^= 1 << (bit % 8)
+        bad = bytes(bad)
+        try:
+            O.decompress(bad)
+            werr = None
+        except O.OracleError as exc:
+            werr = (type(exc).__name__, error_prefix(str(exc)))
+        gerr = _outcome(lambda: gz.decompress(bad))[1]
+        assert gerr == werr, int(bit)
 
 
 def test_large_sampled_block_parity():
