@@ -81,7 +81,8 @@ def test_compress_bound_covers_worst_case():
     assert L.lib.gpzb_compress_bound(1024, 3, 0, 1024, 32, 0, ctypes.byref(b)) == 0
     # 46 + 2 table entries + header + 64-bit deltas/offsets + 11-bit counts
     assert b.value >= 46 + 16 + 50 + 8192 + 1408 + 8192
-    assert L.lib.gpzb_compress_bound(10, 3, 0, 2048, 32, 0, ctypes.byref(b)) == L.UNSUPPORTED
+    assert L.lib.gpzb_compress_bound(10, 3, 0, 2048, 32, 0, ctypes.byref(b)) == 0  # K2b / K4b
+    assert L.lib.gpzb_compress_bound(10, 3, 0, 1 << 25, 32, 0, ctypes.byref(b)) == L.UNSUPPORTED
     assert L.lib.gpzb_compress_bound(10, 3, 0, 100, 32, 0, ctypes.byref(b)) == L.INVALID
 
 
