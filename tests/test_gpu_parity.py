@@ -371,3 +371,22 @@ def test_offset_free_warp_blocks(prec, dims):
         wpos = 8 + dims * (2 * S + 5)
         assert blk[wpos + 2] == 0  # w_off
         assert int.from_bytes(blk[4:8], "little") <= (128 if prec == O.F64 else 256)
+
+
+@pytest.mark.parametrize("mode,pres,prec", [(1, False, O.F32), (0, True, O.F64)])
+def test_remembered_header_matches_container(mode, pres, prec):
+    """compress_device attaches the parsed global header to its result (so a
+    device decode skips the header read); it must equal the header parsed
+    from the container bytes, and an in-place change of the tensor must make
+    decompress read the bytes again."""
+    axes = O.gen_clusters(20_000, dims=3, seed=4, prec=prec)
+    ds = gz.Dataset.from_axes([torch.from_numpy(a).cuda() for a in axes])
+    c = gz.compress_device(ds, _cfg(1e-3, mode, 1024, 32, pres))
+    h1 = gz.pipeline._known_header(c)
+    h2 = gz.pipeline.parse_header(c[:46].cpu().numpy().tobytes(), c.numel())
+    assert h1 is not None
+    assert all(getattr(h1, f) == getattr(h2, f) for f, _ in type(h1)._fields_)
+    c[4] ^= 0xFF  # the version field: the container is now invalid
+    assert gz.pipeline._known_header(c) is None
+    with pytest.raises(gz.CorruptData):
+        gz.decompress_device(c)

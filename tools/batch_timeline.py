@@ -25,7 +25,7 @@ dss, cfg = [j.ds for j in jobs], jobs[0].cfg
 if "rev" in sys.argv:
     dss = dss[::-1]
 marks = []
-names = ["gpzb_workspace_reset_async", "gpzb_range_async", "gpzb_range_background_async", "gpzb_range_finish_async",
+names = ["gpzb_decompress_async", "gpzb_decompress_result", "gpzb_workspace_reset_async", "gpzb_range_async", "gpzb_range_background_async", "gpzb_range_finish_async",
          "gpzb_encode_plan_async", "gpzb_encode_async", "gpzb_emit_async", "gpzb_compress_result"]
 names = [n for n in names if hasattr(_lib.lib, n)]
 orig = {n: getattr(_lib.lib, n) for n in names}
@@ -47,17 +47,23 @@ def wrap(n):
 
 
 for _ in range(3):
-    pipeline.compress_batch_device(dss, cfg)
+    conts = pipeline.compress_batch_device(dss, cfg)
+    pipeline.decompress_batch_device(conts)
 torch.cuda.synchronize()
 for n in names:
     setattr(_lib.lib, n, wrap(n))
     setattr(pipeline.lib, n, getattr(_lib.lib, n))
-t0 = torch.cuda.Event(enable_timing=True)
-t0.record()
-pipeline.compress_batch_device(dss, cfg)
-t1 = torch.cuda.Event(enable_timing=True)
-t1.record()
-torch.cuda.synchronize()
-print(f"total {t0.elapsed_time(t1):.3f} ms")
-for n, sid, e0, e1 in marks:
-    print(f"  stream {sid % 1000:4d} {n:32s} {t0.elapsed_time(e0):7.3f} -> {t0.elapsed_time(e1):7.3f}")
+for label, fn in (("compress_batch_device", lambda: pipeline.compress_batch_device(dss, cfg)),
+                  ("decompress_batch_device", lambda: pipeline.decompress_batch_device(conts))):
+    marks.clear()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    out = fn()
+    t1 = torch.cuda.Event(enable_timing=True)
+    t1.record()
+    torch.cuda.synchronize()
+    if label.startswith("compress"):
+        conts = out
+    print(f"{label}: total {t0.elapsed_time(t1):.3f} ms")
+    for n, sid, e0, e1 in marks:
+        print(f"  stream {sid % 1000:4d} {n:32s} {t0.elapsed_time(e0):7.3f} -> {t0.elapsed_time(e1):7.3f}")
