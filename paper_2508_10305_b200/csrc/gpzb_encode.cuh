@@ -233,6 +233,7 @@ enum : uint8_t { KIND_NARROW = 0, KIND_WIDE = 1, KIND_ERROR = 2, KIND_WARP = 3, 
 // Full float32 blocks with Σ log2 m <= kSmallMaxSumb (16 nibble counters in
 // one u64 per segment rank) take the K2s encoder (gpzb_encode_small.cuh).
 constexpr uint32_t kSmallMaxSumb = 4;
+constexpr uint32_t kSmallMaxPN = 32768;  // ... and Π N <= 2^15
 
 // Narrow blocks the warp encoder K2p takes: full, vector-loadable, no
 // offset stream (every log2 m == 0) and Π N <= 16384.
@@ -309,7 +310,8 @@ __global__ void __launch_bounds__(256) k_geometry(const EncParams P) {
     if (narrow) {
       const uint64_t n = min((uint64_t)P.bs, P.count - blk * (uint64_t)P.bs);
       const bool full = n == (uint64_t)kMaxBs && P.vec;
-      if (full && sizeof(T) == 4 && sumb <= kSmallMaxSumb && P.use_small && (sumb > 0 || P.small0)) {
+      if (full && sizeof(T) == 4 && sumb <= kSmallMaxSumb && PN <= kSmallMaxPN && P.use_small &&
+          (sumb > 0 || P.small0)) {
         // K2s (gpzb_encode_small.cuh): with offsets from the front of the list, offset-free from the back
         rec.kind = KIND_SMALL;
         if (sumb) P.small_list[atomicAdd(&R->small_count, 1u)] = (uint32_t)blk;

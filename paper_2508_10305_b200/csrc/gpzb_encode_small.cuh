@@ -41,7 +41,7 @@
 namespace gpzb {
 
 #ifndef GPZB_K2S_MINB
-#define GPZB_K2S_MINB 6
+#define GPZB_K2S_MINB 7
 #endif
 #ifndef GPZB_K2S0_MINB
 #define GPZB_K2S0_MINB 7
@@ -49,7 +49,10 @@ namespace gpzb {
 constexpr int kST = 128;               // K2s threads per block
 constexpr int kSW = kST / 32;          // warps per block
 constexpr int kSP = kMaxBs / kST;      // particles (and runs) per thread
-constexpr uint32_t kSmallMaxPN = 65536;
+// Π N <= 2^15 (t = 32 in 3D: N_a <= 32 per axis), so the presence bitmap and
+// the stage it becomes are 4 KB; with 30 KB of shared memory per CTA seven
+// CTAs (28 warps) fit an SM
+static_assert(kSmallMaxPN == 32768, "bitmap sizing below");
 // payload <= 50 + 1024 * 16 / 8 + 1024 * 11 / 8 (no offsets) = 3,506 bytes
 // (with offsets: counts <= 8 bits, offsets <= 4 bits: 3,634 bytes)
 constexpr int kSmallStageWords = 1024;
@@ -72,7 +75,7 @@ struct SmallSmem {
   // presence bitmap over segments (quantize .. ranks), then the payload stage
   __align__(16) uint32_t bm[kSmallMaxPN / 32];
   // set bits before each bitmap word (prefix .. ranks), then run starts
-  __align__(16) uint16_t wp[kSmallMaxPN / 32];
+  __align__(16) uint16_t wp[kMaxBs + kMaxBs / 2];  // >= kSmallMaxPN / 32 prefixes; run starts (u16) + offsets (u8)
   // per segment rank r: counter word cnt[r] (offsets 0-7, one nibble each)
   // and cnt[1024 + r] (offsets 8-15); offset-free blocks: the run length
   __align__(16) uint32_t cnt[HAS_OFF ? 2 * kMaxBs : kMaxBs];
