@@ -162,6 +162,9 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
     sm.blk = list_at(blockIdx.x);
     small_fetch<D, HAS_OFF>(P, sm, sm.blk);
   }
+  // thread 0 keeps the list entry of the block after next in a register, read
+  // one block ahead, so issuing the next bulk copy never waits on global memory
+  uint32_t next_blk = (tid == 0 && blockIdx.x + gridDim.x < nlist) ? list_at(blockIdx.x + gridDim.x) : 0u;
   __syncthreads();
 
   const uint32_t bm_s = smem_u32(sm.bm);
@@ -176,6 +179,12 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
     const uint32_t sumb = HAS_OFF ? (uint32_t)sm.rec.sumb : 0u;
     const uint32_t w_hdr_b = HAS_OFF && lane < D ? (uint32_t)sm.rec.b[lane] : 0u;
     const uint32_t w_hdr_n = lane < D ? sm.rec.N[lane] : 0u;
+    // warp 0's header lanes 2 + 4a + {0, 1} write the block's stored bounds:
+    // load them now so the global-memory latency hides behind the quantizer
+    uint32_t w_hdr_bound = 0;
+    if (wid == 0 && lane >= 2 && lane < 2 + 4 * D && ((lane - 2) & 3) < 2)
+      w_hdr_bound = __float_as_uint(
+          reinterpret_cast<const float*>(P.bounds)[(uint64_t)blk * 2 * D + 2 * ((lane - 2) >> 2) + ((lane - 2) & 3)]);
 
     // ---- quantize -> key = seg | off << 16
     uint32_t key[kSP], off_or = 0;
@@ -239,8 +248,9 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
     __syncthreads();  // Bz: coordinates and record consumed; the previous stage is out and zeroed
     if (tid == 0 && item + gridDim.x < nlist) {  // the next block's bulk copy overlaps this block's encode
       fence_proxy_async_smem();
-      sm.blk = list_at(item + gridDim.x);
-      small_fetch<D, HAS_OFF>(P, sm, sm.blk);
+      sm.blk = next_blk;
+      small_fetch<D, HAS_OFF>(P, sm, next_blk);
+      if (item + 2 * gridDim.x < nlist) next_blk = list_at(item + 2 * gridDim.x);
     }
 #pragma unroll
     for (int k = 0; k < kSP; ++k) {
@@ -389,7 +399,7 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
         const uint32_t ab = 8 + a * 13;
         if (which < 2) {
           bpos = ab + which * 4;
-          val = __float_as_uint(reinterpret_cast<const float*>(P.bounds)[(uint64_t)blk * 2 * D + 2 * a + which]);
+          val = w_hdr_bound;
         } else if (which == 2) { bpos = ab + 8; val = hb; }
         else { bpos = ab + 9; val = hn; }
       } else if (f < 2 + 4 * D + 3) {

@@ -34,6 +34,9 @@ constexpr int kWarpEncWarps = GPZB_K2P_WARPS;
 // payload <= 74 + 1024 * (14 + 11) / 8 + 2 = 3,276 bytes (widths <= bitlen(16383), bitlen(1024))
 constexpr int kWarpStageWords = 832;
 struct WarpEncSmem {
+  // the geometry record (128 B) and stored bounds (<= 48 B) of this and the
+  // warp's next block, brought in by 4-byte cp.async one block ahead
+  __align__(16) uint32_t recw[2][32 + 12];
   __align__(16) uint32_t bm[kWarpStageWords];  // presence bitmap (<= 512 words), then the payload stage
   uint16_t wp[kWarpEncMaxPN / 32];             // set bits before each bitmap word
   __align__(16) uint32_t cnt[kMaxBs];          // run length per segment rank
@@ -54,9 +57,28 @@ __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_wa
   uint4 raw[D][4 / VE];      // 16-byte loads of the chunk being (or about to be) quantized
   uint64_t raw_blk = ~0ull;  // block whose chunk 0 sits in raw
   const uint64_t stride = (uint64_t)gridDim.x * kWarpEncWarps;
-  for (uint64_t blk = (uint64_t)blockIdx.x * kWarpEncWarps + wid; blk < P.nblocks; blk += stride) {
+  // the geometry record (one word per lane) and the stored block bounds of
+  // the warp's next block are copied to shared memory one block ahead, so no
+  // block starts (or writes its header) waiting on global memory
+  static_assert(sizeof(BlkRec) == 128, "one record word per lane");
+  constexpr int kBW = 2 * D * (S / 4);  // bound words per block
+  auto prefetch_rec = [&](uint64_t b, int buf) {
+    if (b < P.nblocks) {
+      cp_async4(&sm.recw[buf][lane], reinterpret_cast<const uint32_t*>(P.rec + b) + lane);
+      if (lane < kBW) cp_async4(&sm.recw[buf][32 + lane], reinterpret_cast<const uint32_t*>(P.bounds) + b * kBW + lane);
+    }
+    cp_async_commit();
+  };
+  const uint64_t blk0 = (uint64_t)blockIdx.x * kWarpEncWarps + wid;
+  prefetch_rec(blk0, 0);
+  int buf = 0;
+  for (uint64_t blk = blk0; blk < P.nblocks; blk += stride, buf ^= 1) {
     const BlkRec* rec = P.rec + blk;
-    if (rec->kind != KIND_WARP) continue;  // warp-uniform
+    cp_async_wait_all();
+    __syncwarp();
+    const uint32_t* recw = sm.recw[buf];
+    prefetch_rec(blk + stride, buf ^ 1);
+    if ((reinterpret_cast<const uint8_t*>(recw)[offsetof(BlkRec, kind)]) != KIND_WARP) continue;  // warp-uniform
     const uint64_t first = blk * (uint64_t)P.bs;
 #if GPZB_K2P_L2PF
     // the next block's coordinates into L2 (one bulk prefetch per axis): its
@@ -70,7 +92,7 @@ __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_wa
                      : "memory");
     }
 #endif
-    const uint32_t PN = rec->PN;
+    const uint32_t PN = recw[offsetof(BlkRec, PN) / 4];
     const uint32_t nw = (PN + 31) >> 5;
     // ---- zero the bitmap and the run counters
     for (uint32_t w = lane; w < (nw + 3) >> 2; w += 32) reinterpret_cast<uint4*>(sm.bm)[w] = make_uint4(0, 0, 0, 0);
@@ -83,10 +105,11 @@ __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_wa
       uint32_t st = 1;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        lo[a] = rec->lo[a];
-        rinv[a] = rec->rinv[a];
+        constexpr int kLo = offsetof(BlkRec, lo) / 4, kRi = offsetof(BlkRec, rinv) / 4, kN = offsetof(BlkRec, N) / 4;
+        lo[a] = __hiloint2double((int)recw[kLo + 2 * a + 1], (int)recw[kLo + 2 * a]);
+        rinv[a] = __hiloint2double((int)recw[kRi + 2 * a + 1], (int)recw[kRi + 2 * a]);
         Nst[a] = st;
-        st *= rec->N[a];
+        st *= recw[kN + a];
       }
     }
     __syncwarp();
@@ -236,19 +259,22 @@ __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_wa
       uint32_t bpos = 0;
       uint64_t val = 0;
       bool act = true;
+      // the stored bounds and N of this lane's field, from the prefetched words
+      const int fa = f >= 2 && f < 2 + 4 * D ? (f - 2) >> 2 : 0, fw = (f - 2) & 3;
+      const int bw = (2 * fa + (fw & 1)) * (S / 4);
+      const uint32_t b_lo = recw[32 + bw], b_hi = recw[32 + (S / 4 == 2 ? bw + 1 : bw)];
+      const uint32_t n_a = recw[offsetof(BlkRec, N) / 4 + fa];
       if (f == 0) { bpos = 0; val = (uint32_t)kMaxBs; }
       else if (f == 1) { bpos = 4; val = U; }
       else if (f < 2 + 4 * D) {
         const int a = (f - 2) >> 2, which = (f - 2) & 3;
         const uint32_t ab = 8 + a * (2 * S + 5);
-        const T* bnd = reinterpret_cast<const T*>(P.bounds) + blk * 2 * D;
         if (which < 2) {
           bpos = ab + which * S;
-          const T v = bnd[2 * a + which];
-          if constexpr (F64) val = (uint64_t)__double_as_longlong(v);
-          else val = __float_as_uint(v);
+          if constexpr (F64) val = (uint64_t)b_hi << 32 | b_lo;
+          else val = b_lo;
         } else if (which == 2) { bpos = ab + 2 * S; val = 0; }  // log2 m == 0
-        else { bpos = ab + 2 * S + 1; val = rec->N[a]; }
+        else { bpos = ab + 2 * S + 1; val = n_a; }
       } else if (f < 2 + 4 * D + 3) {
         const int wi = f - 2 - 4 * D;
         bpos = 8 + D * (2 * S + 5) + wi;
