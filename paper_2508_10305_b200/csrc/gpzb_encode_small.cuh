@@ -259,29 +259,22 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
     }
     __syncthreads();  // B1: presence bitmap complete
 
-    // ---- bitmap word prefixes: thread t owns 16-byte groups [t*gpt, t*gpt + gpt)
-    const uint32_t ng = (((PN + 31) >> 5) + 3) >> 2;  // <= 512
-    const uint32_t gpt = (ng + kST - 1) / kST;         // <= 4, block-uniform
+    // ---- bitmap word prefixes: thread t owns the 16-byte groups 2t and 2t + 1
+    static_assert(kSmallMaxPN / 128 == 2 * kST, "two bitmap groups per thread");
+    const uint32_t ng = (((PN + 31) >> 5) + 3) >> 2;  // <= 256
     uint32_t U;
     {
-      uint32_t l = 0;
-      for (uint32_t i = 0; i < gpt; ++i) {
-        const uint32_t g = tid * gpt + i;
-        if (g < ng) {
-          const uint4 q = reinterpret_cast<const uint4*>(sm.bm)[g];
-          l += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
-        }
-      }
-      uint32_t e = small_excl_scan(l, U, sm.scan[0]);  // B2
-      for (uint32_t i = 0; i < gpt; ++i) {
-        const uint32_t g = tid * gpt + i;
-        if (g < ng) {
-          const uint4 q = reinterpret_cast<const uint4*>(sm.bm)[g];
-          const uint32_t e1 = e + __popc(q.x), e2 = e1 + __popc(q.y), e3 = e2 + __popc(q.z);
-          reinterpret_cast<uint2*>(sm.wp)[g] = make_uint2(e | (e1 << 16), e2 | (e3 << 16));
-          e = e3 + __popc(q.w);
-        }
-      }
+      const uint4 z = make_uint4(0, 0, 0, 0);
+      const uint4 q0 = 2 * tid < ng ? reinterpret_cast<const uint4*>(sm.bm)[2 * tid] : z;
+      const uint4 q1 = 2 * tid + 1 < ng ? reinterpret_cast<const uint4*>(sm.bm)[2 * tid + 1] : z;
+      const uint32_t p0 = __popc(q0.x), p1 = __popc(q0.y), p2 = __popc(q0.z), p3 = __popc(q0.w);
+      const uint32_t p4 = __popc(q1.x), p5 = __popc(q1.y), p6 = __popc(q1.z), p7 = __popc(q1.w);
+      const uint32_t e0 = small_excl_scan(p0 + p1 + p2 + p3 + p4 + p5 + p6 + p7, U, sm.scan[0]);  // B2
+      const uint32_t e1 = e0 + p0, e2 = e1 + p1, e3 = e2 + p2, e4 = e3 + p3, e5 = e4 + p4, e6 = e5 + p5,
+                     e7 = e6 + p6;
+      if (2 * tid < ng) reinterpret_cast<uint2*>(sm.wp)[2 * tid] = make_uint2(e0 | (e1 << 16), e2 | (e3 << 16));
+      if (2 * tid + 1 < ng)
+        reinterpret_cast<uint2*>(sm.wp)[2 * tid + 1] = make_uint2(e4 | (e5 << 16), e6 | (e7 << 16));
     }
     __syncthreads();  // B3
 
@@ -343,7 +336,8 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
       }
     }
     // the bitmap becomes the payload stage: zero the words it used
-    for (uint32_t g = tid; g < ng; g += kST) reinterpret_cast<uint4*>(sm.bm)[g] = z4;
+    if (2 * tid < ng) reinterpret_cast<uint4*>(sm.bm)[2 * tid] = z4;
+    if (2 * tid + 1 < ng) reinterpret_cast<uint4*>(sm.bm)[2 * tid + 1] = z4;
     uint32_t total, ex;
     {
       const uint32_t r0 = __reduce_or_sync(kFull, c_or), r1 = __reduce_or_sync(kFull, d_or);
@@ -470,10 +464,14 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
     // the next block's Bz orders this before its bitmap)
     {
       uint4* slot = reinterpret_cast<uint4*>(P.staging + (uint64_t)blk * kSlotBytes);
-      const uint32_t nq = (L + 15) >> 4;
-      for (uint32_t w = tid; w < nq; w += kST) {
-        __stcg(slot + w, reinterpret_cast<const uint4*>(st)[w]);
-        reinterpret_cast<uint4*>(st)[w] = z4;
+      const uint32_t nq = (L + 15) >> 4;  // <= 228 (3,634-byte payloads)
+#pragma unroll
+      for (uint32_t h = 0; h < 2; ++h) {
+        const uint32_t w = tid + h * kST;
+        if (w < nq) {
+          __stcg(slot + w, reinterpret_cast<const uint4*>(st)[w]);
+          reinterpret_cast<uint4*>(st)[w] = z4;
+        }
       }
     }
   }
