@@ -283,23 +283,32 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
       if (r1 > r0 && prev0 + dsum >= PN) fl |= 1u << 13;
       uint32_t uu = (uint32_t)prev0, mn_dl = 0xffffffffu, mn_cn = 0xffffffffu;
       uint32_t cex = (uint32_t)(ex >> kDBits);
-      for (uint32_t r = r0; r < r1; ++r) {
-        uint32_t dl, cn;
-        if (keep) {
-          const uint32_t v = sm.uniq[r];
-          dl = v & 0xffffu;
-          cn = v >> 16;
-        } else {
-          dl = get_bits32(sm.win, pbit + 8 * sd + r * wd, wd);
-          cn = get_bits32(sm.win, pbit + 8 * sc + r * wc, wc);
+      // one loop per block-uniform kind of run record (no per-run branches on
+      // the kind): the run's id (plain), its table bases (wlut) or its values (rv)
+      auto run_loop = [&](auto&& store_run) {
+        for (uint32_t r = r0; r < r1; ++r) {
+          uint32_t dl, cn;
+          if (keep) {
+            const uint32_t v = sm.uniq[r];
+            dl = v & 0xffffu;
+            cn = v >> 16;
+          } else {
+            dl = get_bits32(sm.win, pbit + 8 * sd + r * wd, wd);
+            cn = get_bits32(sm.win, pbit + 8 * sc + r * wc, wc);
+          }
+          uu += dl;
+          mn_dl = min(mn_dl, r ? dl : 0xffffffffu);
+          mn_cn = min(mn_cn, cn);
+          store_run(r, uu);
+          red_or_shared_if(cex < (uint32_t)kMaxBs, &sm.rstart[cex >> 5], 1u << (cex & 31));
+          cex += cn;
         }
-        uu += dl;
-        mn_dl = min(mn_dl, r ? dl : 0xffffffffu);
-        mn_cn = min(mn_cn, cn);
-        if (rv) {
+      };
+      if (rv) {
+        run_loop([&](uint32_t r, uint32_t u) {
           // the run's reconstruction per axis, as the midpoint table would hold it
           T* rvt = reinterpret_cast<T*>(sm.uniq + kWarpLutBase);
-          uint32_t rest = uu;  // u < Π N <= 2^32 (else the block is reported below)
+          uint32_t rest = u;  // u < Π N <= 2^32 (else the block is reported below)
 #pragma unroll
           for (int a = 0; a < D; ++a) {
             uint32_t sa;
@@ -315,9 +324,11 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
             rvt[a * (F64 ? kWarpRvStride / 2 : kWarpRvStride) + r] =
                 (T)__dadd_rn(rec->lo[a], __dmul_rn(__dsub_rn(h, 2251799813685248.0), rec->w[a]));
           }
-          sm.uniq[r] = uu;
-        } else if (wlut) {
-          uint32_t rest = uu, pk = 0;
+          sm.uniq[r] = u;
+        });
+      } else if (wlut) {
+        run_loop([&](uint32_t r, uint32_t u) {
+          uint32_t rest = u, pk = 0;
 #pragma unroll
           for (int a = 0; a < D; ++a) {
             uint32_t sa;
@@ -332,11 +343,9 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
             pk |= ((lb + (sa << rec->b[a])) & 0x3ffu) << (10 * a);
           }
           sm.uniq[r] = pk;
-        } else {
-          sm.uniq[r] = uu;
-        }
-        red_or_shared_if(cex < (uint32_t)kMaxBs, &sm.rstart[cex >> 5], 1u << (cex & 31));
-        cex += cn;
+        });
+      } else {
+        run_loop([&](uint32_t r, uint32_t u) { sm.uniq[r] = u; });
       }
       if (mn_dl == 0) fl |= 1u << 3;  // pipeline.py:116-117
       if (mn_cn == 0) fl |= 1u << 4;  // pipeline.py:118-119
