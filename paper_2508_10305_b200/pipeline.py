@@ -42,9 +42,15 @@ __all__ = [
 _R_NONFINITE, _R_NONFINITE_OUT = 1, 60
 
 
+_CUDA_OK = False
+
+
 def _device() -> torch.device:
-    if not torch.cuda.is_available():
-        raise RuntimeError("the GPZ B200 path needs a CUDA device (there is no CPU fallback)")
+    global _CUDA_OK
+    if not _CUDA_OK:  # checked once: torch.cuda.is_available() reads the environment on every call
+        if not torch.cuda.is_available():
+            raise RuntimeError("the GPZ B200 path needs a CUDA device (there is no CPU fallback)")
+        _CUDA_OK = True
     return torch.device("cuda", torch.cuda.current_device())
 
 
@@ -497,7 +503,9 @@ def _decode_launch(t: torch.Tensor, h: _lib.Header, offsets=None, capacity=None,
     dev = t.device
     if capacity is None:
         capacity = min(h.particle_count, h.block_count * min(h.block_size, _lib.MAX_BLOCK_SIZE))
-    outs = [torch.empty(max(capacity, 1), dtype=prec.torch_dtype, device=dev) for _ in range(h.dims)]
+    # one allocation for every axis (rows 16-byte aligned), one allocator call
+    row = (max(capacity, 1) + 3) & ~3
+    outs = list(torch.empty(h.dims, row, dtype=prec.torch_dtype, device=dev)[:, : max(capacity, 1)].unbind(0))
     ws_bytes = ctypes.c_uint64()
     _check(lib.gpzb_decompress_workspace(ctypes.byref(h), ctypes.byref(ws_bytes)))
     ws = _workspace(ws_bytes.value, slot)
