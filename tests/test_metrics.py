@@ -145,6 +145,27 @@ def test_gpu_pairing_matches_oracle_at_scale():
 
 
 @gpu
+@pytest.mark.parametrize("bs", [2048, 8192])
+def test_gpu_pairing_block_size_above_1024(bs):
+    """K5a's slice-based variant for blocks above 1024 particles: the
+    pairing and the bound report equal the oracle's (metrics.py:49-152)."""
+    gz = _gz()
+    from paper_2508_10305_b200 import metrics as M
+
+    axes = O.gen_clusters(5 * bs + 333, dims=3, seed=bs)
+    cfg = gz.CompressConfig(error_bound=1e-3, block_size=bs)
+    ds = gz.Dataset.from_axes(axes)
+    rec = gz.decompress(gz.compress(ds, cfg))
+    eb_abs = gz.resolve_absolute_bound(ds, cfg)
+    oi, ri = M.pair_blocks(ds, rec, cfg, eb_abs)
+    woi, wri = O.pair_blocks(axes, list(rec.axes), bs, 32, eb_abs)
+    assert np.array_equal(oi, woi) and np.array_equal(ri, wri)
+    rep = M.verify_bound(ds, rec, eb_abs, cfg)
+    m, v, _ = O.verify_bound(axes, list(rec.axes), eb_abs, bs, 32)
+    assert rep.ok and rep.max_err == m and v == []
+
+
+@gpu
 def test_gpu_nrmse_unpaired_and_device_inputs():
     gz = _gz()
     import torch
