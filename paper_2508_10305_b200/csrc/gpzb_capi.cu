@@ -295,7 +295,10 @@ void launch_pair_blocks(const PairParams& P, cudaStream_t s) {
   using T = typename std::conditional<F64, double, float>::type;
   using R = typename std::conditional<R64, double, float>::type;
   GPZB_COUNT_LAUNCH();
-  k_pair_blocks<D, T, R><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
+  if (P.bs > (uint32_t)kMaxBs)
+    k_pair_blocks_big<D, T, R><<<P.big_grid, kThreads, 0, s>>>(P, P.big, big_pad(P.bs), big_enc_slice(P.bs));
+  else
+    k_pair_blocks<D, T, R><<<(unsigned)P.nblocks, kThreads, 0, s>>>(P);
 }
 
 template <int D, bool F64, bool R64>
@@ -982,7 +985,6 @@ int gpzb_pair_blocks(const void* const* orig, const void* const* rec, int dims, 
                      int64_t* rec_idx, void* ws, uint64_t ws_bytes, void* stream, gpzb_result* res) {
   clear_result(res);
   int st = check_args(dims, prec, bs);
-  if (!st && bs > (uint32_t)kMaxBs) st = GPZB_UNSUPPORTED;  // K5a: one CTA holds a whole block
   if (st) return res->status = st;
   if ((rprec != GPZB_F32 && rprec != GPZB_F64) || target == 0 || (target & (target - 1)))
     return res->status = GPZB_INVALID_ARGUMENT;
@@ -1002,8 +1004,19 @@ int gpzb_pair_blocks(const void* const* orig, const void* const* rec, int dims, 
   P.res = reinterpret_cast<DevResult*>(ws);
   cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(DevResult), s);
   if (e != cudaSuccess) return res->status = cuda_status(e);
+  void* big = nullptr;
+  if (bs > (uint32_t)kMaxBs) {
+    // blocks above 1024 particles: per-CTA key slices, the call's one
+    // allocation (stream-ordered pool), freed behind the kernel
+    const uint64_t slice = big_enc_slice(bs), grid = big_grid(P.nblocks, slice);
+    e = cudaMallocAsync(&big, grid * slice, s);
+    if (e != cudaSuccess) return res->status = cuda_status(e);
+    P.big = static_cast<uint8_t*>(big);
+    P.big_grid = (uint32_t)grid;
+  }
   DISPATCH_DPR(dims, prec, rprec, launch_pair_blocks, P, s);
   e = cudaGetLastError();
+  if (big) cudaFreeAsync(big, s);
   DevResult R;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&R, ws, sizeof(R), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);

@@ -233,6 +233,11 @@ enum : uint8_t { KIND_NARROW = 0, KIND_WIDE = 1, KIND_ERROR = 2, KIND_WARP = 3, 
 // Full float32 blocks with Σ log2 m <= kSmallMaxSumb (16 nibble counters in
 // one u64 per segment rank) take the K2s encoder (gpzb_encode_small.cuh).
 constexpr uint32_t kSmallMaxSumb = 4;
+// Added to t * RN(1/w) by the K2s / K2p quantizers' FMA: 2^-60 (1 + 5 * 2^-52),
+// whose low word (5) passes the certificate, so an exact zero (x == block
+// minimum) needs no special case; for r >= 2^-8 it moves the product by
+// < 2^-8 ulp, inside the certificate's two-ulp slack.
+constexpr unsigned long long kCertNudgeBits = 0x3C30000000000005ull;
 constexpr uint32_t kSmallMaxPN = 32768;  // ... and Π N <= 2^15
 
 // Narrow blocks the warp encoder K2p takes: full, vector-loadable, no

@@ -56,11 +56,6 @@ static_assert(kSmallMaxPN == 32768, "bitmap sizing below");
 // payload <= 50 + 1024 * 16 / 8 + 1024 * 11 / 8 (no offsets) = 3,506 bytes
 // (with offsets: counts <= 8 bits, offsets <= 4 bits: 3,634 bytes)
 constexpr int kSmallStageWords = 1024;
-// Added to t * RN(1/w) by the quantizer's FMA: 2^-60 (1 + 5 * 2^-52), whose
-// low word (5) passes the certificate, so an exact zero (x == block minimum)
-// needs no special case; for r >= 2^-8 it moves the product by < 2^-8 ulp,
-// inside the certificate's two-ulp slack.
-constexpr unsigned long long kCertNudgeBits = 0x3C30000000000005ull;
 
 template <int D, bool HAS_OFF>
 struct SmallSmem {

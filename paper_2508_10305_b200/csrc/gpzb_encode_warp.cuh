@@ -147,20 +147,23 @@ __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_wa
         }
       }
       uint32_t seg[4] = {0, 0, 0, 0};
-      bool bad = false;
+      uint32_t mn = ~0u, mx = 0u;  // extremes of the low words: 0 or ~0 flags a possible failure
 #pragma unroll
       for (int a = 0; a < D; ++a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          // certified reciprocal quantizer (gpzb_common.cuh quantize_coord, mode 0)
+          // certified reciprocal quantizer with the FMA nudge (K2s, DESIGN.md
+          // §3.1): t == 0 gives r = nudge, whose low word passes
           const double t = __dsub_rn((double)x[a][k], lo[a]);
-          const double r = __dmul_rn(t, rinv[a]);
-          const uint32_t rl = (uint32_t)__double2loint(r), rh = (uint32_t)__double2hiint(r);
+          const double r = __fma_rn(t, rinv[a], __longlong_as_double((long long)kCertNudgeBits));
+          const uint32_t rl = (uint32_t)__double2loint(r);
           const uint32_t q = (uint32_t)__double2loint(__dadd_rz(r, 4503599627370496.0));
-          bad |= ((rl + 1u) <= 1u) & (rh != 0u);  // r == 0 (t == 0) is exact
+          mn = min(mn, rl);
+          mx = max(mx, rl);
           seg[k] += q * Nst[a];
         }
       }
+      const bool bad = mn == 0u || mx == ~0u;
       if (__any_sync(kFull, bad)) {
         if (bad) {
 #pragma unroll

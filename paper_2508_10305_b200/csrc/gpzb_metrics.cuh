@@ -38,6 +38,8 @@ struct PairParams {
   unsigned long long* viol_count;
   unsigned long long* viol;  // [cap][3]: axis << 56 | position, original index, |error| bits
   uint64_t viol_cap;
+  uint8_t* big;         // K5a for blocks above 1024 particles: per-CTA key slices
+  uint32_t big_grid;
 };
 
 template <typename T>
@@ -193,6 +195,134 @@ __global__ void __launch_bounds__(kThreads) k_pair_blocks(const PairParams P) {
     int64_t* dst = side ? P.rec_idx : P.orig_idx;
     for (int p = tid; p < n; p += kThreads) dst[first + p] = (int64_t)(first + sm.idx[p]);
     __syncthreads();
+  }
+}
+
+// K5a for blocks of more than 1024 particles (gpzb_big.cuh's layout): one
+// CTA per block, persistent; the (seg, off, index) keys of each side in a
+// per-CTA slice of `scratch` (big_enc_slice bytes), padded with all-ones keys
+// to a power of two and bitonic-sorted there; same results as k_pair_blocks.
+template <int D, typename T, typename R>
+__global__ void __launch_bounds__(kThreads) k_pair_blocks_big(const PairParams P, uint8_t* scratch, uint64_t npad,
+                                                              uint64_t slice) {
+  __shared__ unsigned long long red[2 * 3 * kWarps];
+  __shared__ AxisGeo geo[3];
+  __shared__ int serr;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr bool F64 = sizeof(T) == 8;
+  unsigned long long* seg = reinterpret_cast<unsigned long long*>(scratch + blockIdx.x * slice);
+  unsigned long long* off = seg + npad;
+  uint32_t* idx = reinterpret_cast<uint32_t*>(off + npad);
+  for (uint64_t blk = blockIdx.x; blk < P.nblocks; blk += gridDim.x) {
+    __syncthreads();
+    const uint64_t first = blk * (uint64_t)P.bs;
+    const uint32_t n = (uint32_t)min((uint64_t)P.bs, P.count - first);
+    // ---- the original block's bounds (quantizer.block_bounds) and finiteness of both sides
+    unsigned long long kmin[D], kmax[D];
+    uint32_t nf = 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) { kmin[a] = ~0ull; kmax[a] = 0ull; }
+    for (uint32_t p = tid; p < n; p += kThreads) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const T v = reinterpret_cast<const T*>(P.orig[a])[first + p];
+        const T w = (T)reinterpret_cast<const R*>(P.rec[a])[first + p];  // metrics.py:74
+        if (!finite_t(v)) nf |= 1u << a;
+        if (!finite_t(w)) nf |= 1u << (4 + a);
+        const unsigned long long kk = okey((double)v);
+        kmin[a] = min(kmin[a], kk);
+        kmax[a] = max(kmax[a], kk);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      unsigned long long mn = kmin[a], mx = kmax[a];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(kFull, mn, o));
+        mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+      }
+      if (lane == 0) { red[(2 * a) * kWarps + wid] = mn; red[(2 * a + 1) * kWarps + wid] = mx; }
+    }
+    nf = __reduce_or_sync(kFull, nf);
+    if (lane == 0 && nf) atomicOr(&P.res->nonfinite_mask, nf);
+    __syncthreads();
+    if (tid == 0) {
+      int err = R_NONE, eax = 0;
+      if (!(P.eb_abs > 0.0)) err = R_EB_NOT_POSITIVE;
+      unsigned __int128 pn = 1;
+      uint32_t sumb = 0;
+      for (int a = 0; a < D && !err; ++a) {
+        unsigned long long mn = ~0ull, mx = 0ull;
+        for (int w = 0; w < kWarps; ++w) {
+          mn = min(mn, red[(2 * a) * kWarps + w]);
+          mx = max(mx, red[(2 * a + 1) * kWarps + w]);
+        }
+        if (axis_geometry(ukey_inv(mn), ukey_inv(mx), P.eb_abs, F64, P.target, geo[a])) {
+          err = R_AXIS_RANGE;
+          eax = a;
+        } else {
+          pn *= geo[a].N;
+          if (pn > ((unsigned __int128)1 << 64)) pn = ((unsigned __int128)1 << 64) + 1;
+          sumb += geo[a].b;
+        }
+      }
+      if (!err && (pn > ((unsigned __int128)1 << 64) || sumb > 64)) err = R_GEOMETRY;
+      if (err) atomicMax(&P.res->err_block, err_code(blk, eax, err));
+      serr = err;  // non-finite values: reported as DomainError by the host (results discarded)
+    }
+    __syncthreads();
+    if (serr) continue;
+    // ---- each side: keys with the original's geometry, sorted; positional pairs
+    for (int side = 0; side < 2; ++side) {
+      for (uint64_t p = tid; p < npad; p += kThreads) {
+        unsigned long long s = ~0ull, o = ~0ull;
+        uint32_t ix = ~0u;
+        if (p < n) {
+          s = 0;
+          o = 0;
+          ix = (uint32_t)p;
+          unsigned long long stride = 1;
+          uint32_t shift = 0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            const AxisGeo& g = geo[a];
+            const double x = side ? (double)(T)reinterpret_cast<const R*>(P.rec[a])[first + p]
+                                  : (double)reinterpret_cast<const T*>(P.orig[a])[first + p];
+            const uint64_t q = quantize_snap(x, g, P.eb_abs, F64);  // quantizer.py:142-173
+            s += shr64(q, g.b) * stride;                           // quantizer.py:176-191
+            o |= shl64(q & (g.b >= 64 ? ~0ull : ((1ull << g.b) - 1)), shift);
+            stride *= g.N;
+            shift += g.b;
+          }
+        }
+        seg[p] = s;
+        off[p] = o;
+        idx[p] = ix;
+      }
+      __syncthreads();
+      for (uint64_t k = 2; k <= npad; k <<= 1) {
+        for (uint64_t j = k >> 1; j > 0; j >>= 1) {
+          for (uint64_t i = tid; i < npad; i += kThreads) {
+            const uint64_t l = i ^ j;
+            if (l > i) {
+              const unsigned long long s1 = seg[i], o1 = off[i], s2 = seg[l], o2 = off[l];
+              const uint32_t i1 = idx[i], i2 = idx[l];
+              const bool lt21 = s2 < s1 || (s2 == s1 && (o2 < o1 || (o2 == o1 && i2 < i1)));
+              const bool lt12 = s1 < s2 || (s1 == s2 && (o1 < o2 || (o1 == o2 && i1 < i2)));
+              if ((i & k) == 0 ? lt21 : lt12) {
+                seg[i] = s2; off[i] = o2; idx[i] = i2;
+                seg[l] = s1; off[l] = o1; idx[l] = i1;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      int64_t* dst = side ? P.rec_idx : P.orig_idx;
+      for (uint32_t p = tid; p < n; p += kThreads) dst[first + p] = (int64_t)(first + idx[p]);
+      __syncthreads();
+    }
   }
 }
 
