@@ -338,6 +338,13 @@ __device__ __forceinline__ uint64_t quantize_coord(double x, const AxisGeo& g, d
   return quantize_snap(x, g, eb, f64);
 }
 
+// (1 << (w mod 32)) - 1 in one instruction (BMSK)
+__device__ __forceinline__ uint32_t bmsk_wrap(uint32_t w) {
+  uint32_t d;
+  asm("bmsk.wrap.b32 %0, 0, %1;" : "=r"(d) : "r"(w));
+  return d;
+}
+
 // ------------------------------------------------------ staging bit writer
 // OR `nbits` (<= 64) bits of v into a u32 word array at bit position pos.
 __device__ __forceinline__ void or_bits(uint32_t* st, uint64_t pos, uint64_t v) {

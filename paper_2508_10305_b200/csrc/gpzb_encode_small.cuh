@@ -78,12 +78,6 @@ struct SmallSmem {
 };
 static_assert(kSmallStageWords <= kSmallMaxPN / 32, "the stage reuses the bitmap");
 
-// (1 << (w mod 32)) - 1 in one instruction (BMSK)
-__device__ __forceinline__ uint32_t bmsk_wrap(uint32_t w) {
-  uint32_t d;
-  asm("bmsk.wrap.b32 %0, 0, %1;" : "=r"(d) : "r"(w));
-  return d;
-}
 
 // Exclusive scan of one value per thread over the (kSW-warp) CTA with a
 // single barrier.  `ws` (16-byte aligned) is not rewritten before a later
