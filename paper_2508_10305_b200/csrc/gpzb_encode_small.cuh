@@ -190,8 +190,11 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
         const uint32_t mks = ((1u << b) - 1u) << shift;
         float x[kSP];
         {
-          const float4 v0 = reinterpret_cast<const float4*>(sm.x[a])[tid];
-          const float4 v1 = reinterpret_cast<const float4*>(sm.x[a])[kST + tid];
+          // particles 8t..8t+7: a warp's quantize step spans 256 consecutive
+          // particles (stride 8), so same-segment neighbours in spatially
+          // ordered data (LiDAR scan lines) collide less in the counter atomics
+          const float4 v0 = reinterpret_cast<const float4*>(sm.x[a])[2 * tid];
+          const float4 v1 = reinterpret_cast<const float4*>(sm.x[a])[2 * tid + 1];
           x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
           x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
         }
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
       if (__any_sync(kFull, bad) && bad) {
 #pragma unroll
         for (int k = 0; k < kSP; ++k) {
-          auto xat = [&](int a) -> float { return sm.x[a][(k < 4 ? 4 * tid : 4 * (kST + tid)) + (k & 3)]; };
+          auto xat = [&](int a) -> float { return sm.x[a][8 * tid + k]; };
           const uint64_t so = redo_exact<D, float>(xat(0), D > 1 ? xat(D > 1 ? 1 : 0) : 0.f,
                                                    D > 2 ? xat(D > 2 ? 2 : 0) : 0.f, &sm.rec);
           seg[k] = (uint32_t)(so >> 32);
