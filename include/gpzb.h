@@ -287,7 +287,8 @@ int gpzb_pair_workspace(uint64_t count, int dims, uint64_t* ws_bytes);
  * the positional pairing as global indices into orig_idx / rec_idx (int64,
  * `count` each).  Synchronous; errors as in compression (non-finite axis:
  * DomainError with the axis, original first; geometry: WidthOverflow with
- * the first failing block). */
+ * the first failing block).  block_size > 1024: the sort keys live in one
+ * stream-ordered scratch allocation of this call (cudaMallocAsync). */
 int gpzb_pair_blocks(const void* const* orig, const void* const* rec, int dims, int precision,
                      int rec_precision, uint64_t count, double eb_abs, uint32_t block_size,
                      uint32_t target_segs_per_axis, int64_t* orig_idx, int64_t* rec_idx, void* ws,
