@@ -419,7 +419,10 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
         const uint32_t r = rk[k] & 0x3ffu, o = rk[k] >> 14;
         const uint32_t m = bmsk_wrap(4 * o);  // nibbles below o's (o & 7)
         uint32_t below;
-        if (wide) {
+        if (wide && short_runs) {  // runs <= 15: every partial nibble sum fits one multiply
+          const uint32_t c0 = sm.cnt[r];
+          below = o < 8 ? nib_sum1(c0 & m) : nib_sum1(c0) + nib_sum1(sm.cnt[1024 | r] & m);
+        } else if (wide) {
           const uint32_t c0 = sm.cnt[r];
           below = o < 8 ? nib_sum8(c0 & m) : nib_sum8(c0) + nib_sum8(sm.cnt[1024 | r] & m);
         } else if (short_runs) {
