@@ -124,7 +124,4 @@ def reason_message(code: int) -> str:
 
 
 def ptr_array(ptrs):
-    arr = (ctypes.c_void_p * max(1, len(ptrs)))()
-    for i, p in enumerate(ptrs):
-        arr[i] = p
-    return arr
+    return (ctypes.c_void_p * max(1, len(ptrs)))(*ptrs)

@@ -475,9 +475,9 @@ def parse_header(head: bytes, container_len: int) -> _lib.Header:
 def _to_device_bytes(data) -> tuple[torch.Tensor, _lib.Header]:
     if isinstance(data, torch.Tensor):
         known = _known_header(data) if data.is_cuda else None
+        if known is not None:  # compress_device's own 1-D uint8 result
+            return data, known
         t = data.reshape(-1).view(torch.uint8)
-        if known is not None:
-            return t, known
         if not t.is_cuda:
             t = t.to(_device(), non_blocking=True)
         head = t[: _lib.GLOBAL_HEADER_SIZE].cpu().numpy().tobytes()
@@ -497,22 +497,31 @@ def _to_device_bytes(data) -> tuple[torch.Tensor, _lib.Header]:
     return t, h
 
 
-def _decode_launch(t: torch.Tensor, h: _lib.Header, offsets=None, capacity=None, timing=None, slot: int = 0):
+def _decode_launch(t: torch.Tensor, h: _lib.Header, offsets=None, capacity=None, timing=None, slot: int = 0,
+                   stream: int | None = None):
     """Enqueue K4a + K4w + the list decoder; returns what _decode_result needs."""
     prec = Precision(h.precision)
-    dev = t.device
     if capacity is None:
         capacity = min(h.particle_count, h.block_count * min(h.block_size, _lib.MAX_BLOCK_SIZE))
     # one allocation for every axis (rows 16-byte aligned), one allocator call
-    row = (max(capacity, 1) + 3) & ~3
-    outs = list(torch.empty(h.dims, row, dtype=prec.torch_dtype, device=dev)[:, : max(capacity, 1)].unbind(0))
-    ws_bytes = ctypes.c_uint64()
-    _check(lib.gpzb_decompress_workspace(ctypes.byref(h), ctypes.byref(ws_bytes)))
-    ws = _workspace(ws_bytes.value, slot)
-    stream = _stream()
+    cap1 = max(capacity, 1)
+    row = (cap1 + 3) & ~3
+    big = torch.empty(h.dims * row, dtype=prec.torch_dtype, device=t.device)
+    outs = [big[a * row: a * row + cap1] for a in range(h.dims)]
+    base, item = big.data_ptr(), big.element_size()
+    wkey = (h.block_count, h.block_size)
+    wcache = _tls("dec_ws_bytes")
+    ws_bytes = wcache.get(wkey)
+    if ws_bytes is None:
+        v = ctypes.c_uint64()
+        _check(lib.gpzb_decompress_workspace(ctypes.byref(h), ctypes.byref(v)))
+        ws_bytes = wcache[wkey] = v.value
+    ws = _workspace(ws_bytes, slot)
+    if stream is None:
+        stream = _stream()
     e0 = _ev() if timing is not None else None
     _check(lib.gpzb_decompress_async(t.data_ptr(), t.numel(), ctypes.byref(h),
-                                     _lib.ptr_array([o.data_ptr() for o in outs]), capacity,
+                                     _lib.ptr_array([base + a * row * item for a in range(h.dims)]), capacity,
                                      offsets.data_ptr() if offsets is not None else None, ws.data_ptr(),
                                      ws.numel(), stream))
     if timing is not None:
@@ -543,7 +552,7 @@ def decompress_batch_device(containers, *, timing=None) -> list:
         s.wait_event(start)
         with torch.cuda.stream(s):
             t, h = _to_device_bytes(data)
-            launched.append(_decode_launch(t, h, timing=timing, slot=i))
+            launched.append(_decode_launch(t, h, timing=timing, slot=i, stream=s.cuda_stream))
     out = []
     for i, L in enumerate(launched):
         s = _side_stream(i)
