@@ -209,6 +209,8 @@ BIG_CASES = [  # (kind, dims, dtype, eb, mode, block_size, target, preserve_orde
     ("lattice", 1, np.float32, 1e-4, 0, 8192, 64, True, 2 * 8192 + 5),
     ("uniform", 3, np.float32, 1e-7, 1, 2048, 32, False, 2048 + 3),  # half-bound axes / wide keys
     ("clusters", 2, np.float64, 1e-9, 1, 65536, 32, False, 65536 + 999),
+    ("uniform", 3, np.float64, 1e-6, 1, 2048, 16, True, 3 * 2048 + 7),  # F64 + rank stream
+    ("clusters", 3, np.float32, 1e-12, 0, 4096, 32, False, 4096 + 5),  # WidthOverflow (oracle: error)
 ]
 
 
@@ -237,6 +239,34 @@ def test_block_size_above_1024(case_):
     assert len(blocks) == (n + bs - 1) // bs
     for a in range(dims):
         assert np.array_equal(np.concatenate([b[a] for b in blocks]), rec.axes[a])
+
+
+def test_block_size_above_1024_streamed_decode():
+    """A > 32 MiB host container of 4096-particle blocks takes the chunked
+    host decode (block ranges through K4b); values equal the one-shot device
+    decode's, and the container equals the oracle's on sampled blocks."""
+    n = 40 * 1024 * 1024 + 123
+    g = torch.Generator(device="cuda").manual_seed(3)
+    pts = torch.rand(n, 3, device="cuda", dtype=torch.float64, generator=g)
+    axes = [pts[:, a].float().contiguous() for a in range(3)]
+    del pts
+    cfg = gz.CompressConfig(error_bound=1e-5, block_size=4096)
+    c = gz.compress_device(gz.Dataset.from_axes(axes), cfg)
+    blob = bytes(c.cpu().numpy())
+    assert len(blob) >= 32 << 20
+    host = gz.decompress(blob)
+    dev = gz.decompress_device(c)
+    for x, y in zip(host.axes, dev.axes):
+        assert np.array_equal(x, y.cpu().numpy())
+    h, table, payload = O.read_container(blob)
+    glob_eb = h.eb_abs  # the dataset's resolved bound, as the container records it
+    rng = np.random.default_rng(1)
+    nb = (n + 4095) // 4096
+    for b in list(rng.integers(0, nb, 12)) + [0, nb - 1]:
+        lo, hi = int(b) * 4096, min((int(b) + 1) * 4096, n)
+        want = O.encode_block([a[lo:hi].cpu().numpy() for a in axes], glob_eb, O.Config(1e-5, block_size=4096),
+                              O.F32)
+        assert bytes(payload[table[b]:table[b + 1]]) == want, int(b)
 
 
 def test_block_size_above_1024_corruption():
