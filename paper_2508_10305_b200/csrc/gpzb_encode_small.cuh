@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
       }
 #pragma unroll
       for (int k = 0; k < kSP; ++k) {
-        key[k] = seg[k] | (off[k] << 16);
+        key[k] = seg[k] | (off[k] << 18);  // seg | (4 * off) << 16: the offset's nibble position
         off_or |= off[k];
       }
     }
@@ -271,21 +271,28 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
     __syncthreads();  // B3
 
     // ---- segment ranks -> counters (tie index returned), unique ids
+    // rk = rank | tie index << 10 | 4 * offset << 14
     uint32_t rk[kSP];
+    auto rank_all = [&](auto wide_c) {
+      constexpr bool WIDE = decltype(wide_c)::value;
 #pragma unroll
-    for (int k = 0; k < kSP; ++k) {
-      const uint32_t sg = key[k] & 0xffffu, w = sg >> 5;
-      const uint32_t r = (uint32_t)sm.wp[w] + __popc(sm.bm[w] & bmsk_wrap(sg));
-      sm.uniq[r + 1] = (uint16_t)sg;
-      if (HAS_OFF) {
-        const uint32_t o = key[k] >> 16, sh = 4 * (o & 7);
-        const uint32_t old = atomicAdd(&sm.cnt[r | (o >> 3) << 10], 1u << sh);
-        rk[k] = r | ((old >> sh) & 15u) << 10 | o << 14;
-      } else {
-        atomicAdd(&sm.cnt[r], 1u);  // result unused: RED
-        rk[k] = r;
+      for (int k = 0; k < kSP; ++k) {
+        const uint32_t sg = key[k] & 0xffffu, w = sg >> 5;
+        const uint32_t r = (uint32_t)sm.wp[w] + __popc(sm.bm[w] & bmsk_wrap(sg));
+        sm.uniq[r + 1] = (uint16_t)sg;
+        if (HAS_OFF) {
+          const uint32_t o4 = key[k] >> 16;  // 4 * offset
+          const uint32_t sh = WIDE ? (o4 & 31u) : o4;
+          const uint32_t old = atomicAdd(&sm.cnt[WIDE ? (r | (o4 >> 5) << 10) : r], 1u << sh);
+          rk[k] = r | ((old >> sh) & 15u) << 10 | o4 << 14;
+        } else {
+          atomicAdd(&sm.cnt[r], 1u);  // result unused: RED
+          rk[k] = r;
+        }
       }
-    }
+    };
+    if (HAS_OFF && sumb > 3) rank_all(std::true_type{});  // counters in both words of a rank
+    else rank_all(std::false_type{});
     __syncthreads();  // B4: bitmap and word prefixes dead
 
     // ---- runs 8t..8t+7: counts, deltas; run starts (scan) and stream widths (OR)
@@ -416,21 +423,21 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
       uint8_t* soff = reinterpret_cast<uint8_t*>(sm.wp + kMaxBs);
 #pragma unroll
       for (int k = 0; k < kSP; ++k) {
-        const uint32_t r = rk[k] & 0x3ffu, o = rk[k] >> 14;
-        const uint32_t m = bmsk_wrap(4 * o);  // nibbles below o's (o & 7)
+        const uint32_t r = rk[k] & 0x3ffu, o4 = rk[k] >> 14;
+        const uint32_t m = bmsk_wrap(o4);  // nibbles below the offset's (mod 32)
         uint32_t below;
         if (wide && short_runs) {  // runs <= 15: every partial nibble sum fits one multiply
           const uint32_t c0 = sm.cnt[r];
-          below = o < 8 ? nib_sum1(c0 & m) : nib_sum1(c0) + nib_sum1(sm.cnt[1024 | r] & m);
+          below = o4 < 32 ? nib_sum1(c0 & m) : nib_sum1(c0) + nib_sum1(sm.cnt[1024 | r] & m);
         } else if (wide) {
           const uint32_t c0 = sm.cnt[r];
-          below = o < 8 ? nib_sum8(c0 & m) : nib_sum8(c0) + nib_sum8(sm.cnt[1024 | r] & m);
+          below = o4 < 32 ? nib_sum8(c0 & m) : nib_sum8(c0) + nib_sum8(sm.cnt[1024 | r] & m);
         } else if (short_runs) {
           below = nib_sum1(sm.cnt[r] & m);  // runs <= 15: one multiply
         } else {
           below = nib_sum8(sm.cnt[r] & m);
         }
-        soff[(uint32_t)sm.wp[r] + below + ((rk[k] >> 10) & 15u)] = (uint8_t)o;
+        soff[(uint32_t)sm.wp[r] + below + ((rk[k] >> 10) & 15u)] = (uint8_t)(o4 >> 2);
       }
       __syncthreads();  // B7
       if (w_off) {  // sorted offsets 8t..8t+7 (each < 16): one 32-bit window
