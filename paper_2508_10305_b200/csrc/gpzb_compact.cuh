@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_sizes(const CompactParams
 // alignment) with lanes [lane, lane + nl, ...) of a warp.  Destination
 // chunks that the payload owns outright get one 16-byte store; the first and
 // last chunk, shared with the neighbouring payloads, get word / byte stores.
-__device__ __forceinline__ void slot_copy(uint8_t* dst, const uint4* src, uint32_t len, int lane, int nl) {
+__device__ __forceinline__ void slot_copy(uint8_t* __restrict__ dst, const uint4* __restrict__ src, uint32_t len, int lane,
+                                          int nl) {
   const uint32_t al = (uint32_t)((uintptr_t)dst & 15);
   uint8_t* g16 = dst - al;
   const uint32_t nbytes = al + len;
@@ -162,6 +163,7 @@ __device__ __forceinline__ void slot_copy(uint8_t* dst, const uint4* src, uint32
   // tail of source chunk c-1 (from byte 16 - al) and the head of chunk c
   const uint32_t o = (16 - al) & 15;
   const uint32_t k = o >> 2, sh = (o & 3) * 8;
+#pragma unroll 2
   for (uint32_t c = lane; c < nch; c += nl) {
     uint32_t w[4];
     if (al == 0) {
