@@ -56,6 +56,13 @@ static_assert(kSmallMaxPN == 32768, "bitmap sizing below");
 // payload <= 50 + 1024 * 16 / 8 + 1024 * 11 / 8 (no offsets) = 3,506 bytes
 // (with offsets: counts <= 8 bits, offsets <= 4 bits: 3,634 bytes)
 constexpr int kSmallStageWords = 1024;
+// particle k of lane l in warp w: lane l owns the 32-particle chunk l, rotated
+// by 8w + k + l so a warp's scalar loads hit 32 distinct banks; one quantize
+// step of a warp spans the whole block (stride 32), which spreads spatially
+// ordered same-segment particles (LiDAR scan lines) across the counter atomics
+__device__ __forceinline__ uint32_t small_pidx(uint32_t lane, uint32_t wid, int k) {
+  return 32u * lane + ((8u * wid + (uint32_t)k + lane) & 31u);
+}
 
 template <int D, bool HAS_OFF>
 struct SmallSmem {
@@ -189,15 +196,8 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
         const uint32_t b = HAS_OFF ? (uint32_t)sm.rec.b[a] : 0u;
         const uint32_t mks = ((1u << b) - 1u) << shift;
         float x[kSP];
-        {
-          // particles 8t..8t+7: a warp's quantize step spans 256 consecutive
-          // particles (stride 8), so same-segment neighbours in spatially
-          // ordered data (LiDAR scan lines) collide less in the counter atomics
-          const float4 v0 = reinterpret_cast<const float4*>(sm.x[a])[2 * tid];
-          const float4 v1 = reinterpret_cast<const float4*>(sm.x[a])[2 * tid + 1];
-          x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
-          x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
-        }
+#pragma unroll
+        for (int k = 0; k < kSP; ++k) x[k] = sm.x[a][small_pidx(lane, wid, k)];
 #pragma unroll
         for (int k = 0; k < kSP; ++k) {
           // certified reciprocal quantizer (gpzb_common.cuh quantize_coord,
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
       if (__any_sync(kFull, bad) && bad) {
 #pragma unroll
         for (int k = 0; k < kSP; ++k) {
-          auto xat = [&](int a) -> float { return sm.x[a][8 * tid + k]; };
+          auto xat = [&](int a) -> float { return sm.x[a][small_pidx(lane, wid, k)]; };
           const uint64_t so = redo_exact<D, float>(xat(0), D > 1 ? xat(D > 1 ? 1 : 0) : 0.f,
                                                    D > 2 ? xat(D > 2 ? 2 : 0) : 0.f, &sm.rec);
           seg[k] = (uint32_t)(so >> 32);
