@@ -56,12 +56,16 @@ static_assert(kSmallMaxPN == 32768, "bitmap sizing below");
 // payload <= 50 + 1024 * 16 / 8 + 1024 * 11 / 8 (no offsets) = 3,506 bytes
 // (with offsets: counts <= 8 bits, offsets <= 4 bits: 3,634 bytes)
 constexpr int kSmallStageWords = 1024;
-// particle k of lane l in warp w: lane l owns the 32-particle chunk l, rotated
-// by 8w + k + l so a warp's scalar loads hit 32 distinct banks; one quantize
-// step of a warp spans the whole block (stride 32), which spreads spatially
-// ordered same-segment particles (LiDAR scan lines) across the counter atomics
+// particles of lane l in warp w: two 4-particle groups of the 32-particle
+// chunk l, groups g0 = (l + 2w) mod 8 and g0 + 1 (mod 8). One quantize step of
+// a warp spans the whole block (stride 32), which spreads spatially ordered
+// same-segment particles (LiDAR scan lines) across the counter atomics, and
+// each 8-lane phase of a 16-byte load covers all 32 banks
+__device__ __forceinline__ uint32_t small_group(uint32_t lane, uint32_t wid, uint32_t h) {
+  return 8u * lane + ((lane + 2u * wid + h) & 7u);  // float4 index
+}
 __device__ __forceinline__ uint32_t small_pidx(uint32_t lane, uint32_t wid, int k) {
-  return 32u * lane + ((8u * wid + (uint32_t)k + lane) & 31u);
+  return 4u * small_group(lane, wid, (uint32_t)k >> 2) + ((uint32_t)k & 3u);
 }
 
 template <int D, bool HAS_OFF>
@@ -190,14 +194,19 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
       for (int k = 0; k < kSP; ++k) { seg[k] = 0; off[k] = 0; }
       uint32_t mn = ~0u, mx = 0u;  // extremes of the low words: 0 or ~0 flags a possible failure
       uint32_t stride = 1, shift = 0;
+      const uint32_t g0 = small_group(lane, wid, 0), g1 = small_group(lane, wid, 1);
 #pragma unroll
       for (int a = 0; a < D; ++a) {
         const double lo = sm.rec.lo[a], rinv = sm.rec.rinv[a];
         const uint32_t b = HAS_OFF ? (uint32_t)sm.rec.b[a] : 0u;
         const uint32_t mks = ((1u << b) - 1u) << shift;
         float x[kSP];
-#pragma unroll
-        for (int k = 0; k < kSP; ++k) x[k] = sm.x[a][small_pidx(lane, wid, k)];
+        {
+          const float4 v0 = reinterpret_cast<const float4*>(sm.x[a])[g0];
+          const float4 v1 = reinterpret_cast<const float4*>(sm.x[a])[g1];
+          x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
+          x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
+        }
 #pragma unroll
         for (int k = 0; k < kSP; ++k) {
           // certified reciprocal quantizer (gpzb_common.cuh quantize_coord,
