@@ -63,7 +63,7 @@ struct DevResult {
   unsigned int warp_count;          // K1.5: blocks for the warp encoder
   unsigned int small_count;         // K1.5: blocks for K2s with offsets (small_list from the front)
   unsigned int small0_count;        // K1.5: blocks for K2s without offsets (small_list from the back)
-  unsigned int pad_;
+  unsigned int claim;               // decode: K4w's next block (zeroed by K4a)
 };
 static_assert(sizeof(DevResult) % 16 == 0, "DevResult alignment");
 

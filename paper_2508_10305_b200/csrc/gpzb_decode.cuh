@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(256) k_decode_plan(const DecParams P) {
   const uint64_t blk = P.blk_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (blk >= P.blk_hi) return;
   DevResult* R = P.res;
+  if (blk == P.blk_lo) R->claim = 0;  // K4w runs after this launch (same stream)
   DecRec rec;
   memset(&rec, 0, sizeof(rec));
   rec.kind = 1;

@@ -162,19 +162,16 @@ __device__ __forceinline__ uint32_t warp_particles(const DecParams& P, const War
   return offbad;
 }
 
+// One block of K4w (one warp): window, runs, particles.
 template <int D, bool F64>
-__global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_warp(const DecParams P) {
+__device__ __forceinline__ void warp_decode_block(const DecParams& P, WarpDecSmem& sm, const uint64_t blk,
+                                                  const int lane) {
   using T = typename std::conditional<F64, double, float>::type;
-  extern __shared__ __align__(16) unsigned char dsm[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  WarpDecSmem& sm = reinterpret_cast<WarpDecSmem*>(dsm)[wid];
   DevResult* R = P.res;
   const uint8_t* cend = P.c + P.len;
-
-  for (uint64_t blk = P.blk_lo + (uint64_t)blockIdx.x * kWarpDecWarps + wid; blk < P.blk_hi;
-       blk += (uint64_t)gridDim.x * kWarpDecWarps) {
+  {
     const DecRec* rec = P.rec + blk;
-    if (rec->kind != 2) continue;  // warp-uniform
+    if (rec->kind != 2) return;  // warp-uniform
     const uint32_t U = rec->U;
     const uint32_t wd = rec->wd, wc = rec->wc, wo = rec->wo;
     const uint32_t sd = rec->sd, sc = rec->sc, so = rec->so;
@@ -355,7 +352,7 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
     if (fl) {
       if (lane == 0) report_decode_error(R, blk, fl);
       __syncwarp();
-      continue;
+      return;
     }
     __syncwarp();
     // ---- run-start map prefix: lane w holds the starts before word w
@@ -399,6 +396,24 @@ __global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_wa
                                                      bsh, shifts, Nn, mgm, mgl, omask);
     if (__any_sync(kFull, offbad != 0) && lane == 0) report_decode_error(R, blk, 1u << 14);
     __syncwarp();
+  }
+}
+
+// K4w: one warp per fast-body block, persistent CTAs.  Blocks are claimed one
+// at a time from a counter (one block ahead, so the atomic's latency hides
+// behind the current block): CTAs that start late (another kernel holds the
+// SMs) still leave the work balanced.
+template <int D, bool F64>
+__global__ void __launch_bounds__(32 * kWarpDecWarps, GPZB_K4W_MINB) k_decode_warp(const DecParams P) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpDecSmem& sm = reinterpret_cast<WarpDecSmem*>(dsm)[wid];
+  unsigned int* claim = &P.res->claim;
+  const uint32_t nblk = (uint32_t)(P.blk_hi - P.blk_lo);
+  uint32_t i = lane == 0 ? atomicAdd(claim, 1u) : 0u, nxt = 0;
+  for (i = __shfl_sync(kFull, i, 0); i < nblk; i = __shfl_sync(kFull, nxt, 0)) {
+    if (lane == 0) nxt = atomicAdd(claim, 1u);
+    warp_decode_block<D, F64>(P, sm, P.blk_lo + i, lane);
   }
 }
 

@@ -1,13 +1,15 @@
 """Per-source-line warp-instruction counts for ONE function of an
-`ncu --page source --csv --print-source cuda,sass` dump (first report of that
-function only), all files, normalised by a count (e.g. warp-blocks):
+`ncu --page source --csv --print-source cuda,sass` dump (the OCC-th report of
+that function, default 1), all files, normalised by a count (e.g. warp-blocks):
 tools/ncu_func_lines.py src.csv '<function substring>' norm [top]"""
 import csv
+import os
 import sys
 
 path, fsub, norm = sys.argv[1], sys.argv[2], float(sys.argv[3])
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 60
-cur_file, cur_fn, hdr, seen, out = "?", None, None, set(), {}
+cur_file, cur_fn, hdr, seen_n, out = "?", None, None, {}, {}
+OCC = int(os.environ.get("OCC", "1"))  # which report of the function
 active = False
 for r in csv.reader(open(path)):
     if len(r) == 2 and r[0] == "File Path":
@@ -15,8 +17,8 @@ for r in csv.reader(open(path)):
         continue
     if len(r) == 2 and r[0] == "Function Name":
         key = (r[1], cur_file)
-        active = fsub in r[1] and key not in seen
-        seen.add(key)
+        seen_n[key] = seen_n.get(key, 0) + 1
+        active = fsub in r[1] and seen_n[key] == OCC
         continue
     if r and r[0] == "Line No":
         hdr = r
