@@ -499,16 +499,15 @@ def _to_device_bytes(data) -> tuple[torch.Tensor, _lib.Header]:
 
 def _decode_launch(t: torch.Tensor, h: _lib.Header, offsets=None, capacity=None, timing=None, slot: int = 0,
                    stream: int | None = None):
-    """Enqueue K4a + K4w + the list decoder; returns what _decode_result needs."""
-    prec = Precision(h.precision)
+    """Enqueue K4a + K4w + the list decoder; returns what _decode_result needs
+    (the output views are cut after the launch: the GPU starts sooner)."""
     if capacity is None:
         capacity = min(h.particle_count, h.block_count * min(h.block_size, _lib.MAX_BLOCK_SIZE))
     # one allocation for every axis (rows 16-byte aligned), one allocator call
     cap1 = max(capacity, 1)
     row = (cap1 + 3) & ~3
-    big = torch.empty(h.dims * row, dtype=prec.torch_dtype, device=t.device)
-    outs = [big[a * row: a * row + cap1] for a in range(h.dims)]
-    base, item = big.data_ptr(), big.element_size()
+    big = torch.empty(h.dims * row, dtype=_DTYPES[h.precision], device=t.device)
+    base, rb = big.data_ptr(), row * big.element_size()
     wkey = (h.block_count, h.block_size)
     wcache = _tls("dec_ws_bytes")
     ws_bytes = wcache.get(wkey)
@@ -521,18 +520,23 @@ def _decode_launch(t: torch.Tensor, h: _lib.Header, offsets=None, capacity=None,
         stream = _stream()
     e0 = _ev() if timing is not None else None
     _check(lib.gpzb_decompress_async(t.data_ptr(), t.numel(), ctypes.byref(h),
-                                     _lib.ptr_array([base + a * row * item for a in range(h.dims)]), capacity,
+                                     _lib.ptr_array([base + a * rb for a in range(h.dims)]), capacity,
                                      offsets.data_ptr() if offsets is not None else None, ws.data_ptr(),
                                      ws.numel(), stream))
     if timing is not None:
         timing.setdefault("decode", []).append((e0, _ev()))
+    outs = [big[a * row: a * row + cap1] for a in range(h.dims)]
     return outs, ws, h, capacity
 
 
-def _decode_result(launched):
+_DTYPES = {p.value: p.torch_dtype for p in Precision}
+
+
+def _decode_result(launched, stream: int | None = None):
     outs, ws, h, capacity = launched
     res = _lib.Result()
-    lib.gpzb_decompress_result(ws.data_ptr(), ws.numel(), ctypes.byref(h), _stream(), ctypes.byref(res))
+    lib.gpzb_decompress_result(ws.data_ptr(), ws.numel(), ctypes.byref(h), _stream() if stream is None else stream,
+                               ctypes.byref(res))
     return outs, res, capacity
 
 
@@ -542,28 +546,36 @@ def _decode(t: torch.Tensor, h: _lib.Header, offsets=None, capacity=None, timing
 
 def decompress_batch_device(containers, *, timing=None) -> list:
     """Decode several containers with one CUDA stream and workspace each
-    (overlapping their kernels); returns Datasets of CUDA tensors in order."""
+    (overlapping their kernels); returns Datasets of CUDA tensors in order.
+    The host work is arranged around the GPU's: every decode is enqueued
+    before any output view or Dataset is built, and those are built before
+    the first result read, so little host time is left on the critical path
+    at either end of the call."""
     cur = torch.cuda.current_stream()
     start = torch.cuda.Event()
     start.record(cur)
-    launched = []
+    launched, streams = [], []
     for i, data in enumerate(containers):
         s = _side_stream(i)
         s.wait_event(start)
-        with torch.cuda.stream(s):
-            t, h = _to_device_bytes(data)
-            launched.append(_decode_launch(t, h, timing=timing, slot=i, stream=s.cuda_stream))
+        known = _known_header(data) if isinstance(data, torch.Tensor) and data.is_cuda else None
+        if known is not None:
+            t, h = data, known
+        else:
+            with torch.cuda.stream(s):
+                t, h = _to_device_bytes(data)
+        # outputs are allocated on `cur` (the caller's stream): cur waits for s
+        # below before anything on it can touch them
+        launched.append(_decode_launch(t, h, timing=timing, slot=i, stream=s.cuda_stream))
+        streams.append(s)
     out = []
-    for i, L in enumerate(launched):
-        s = _side_stream(i)
-        with torch.cuda.stream(s):
-            outs, res, _ = _decode_result(L)
-            _check(res.status, res)
+    for s, (outs, _, h, _) in zip(streams, launched):
         cur.wait_stream(s)
-        for o in outs:
-            o.record_stream(cur)
-        n = L[2].particle_count
-        out.append(Dataset(axes=tuple(o[:n] for o in outs), precision=Precision(L[2].precision)))
+        n = h.particle_count
+        out.append(Dataset._trusted(tuple(o if o.numel() == n else o[:n] for o in outs), Precision(h.precision)))
+    for s, L in zip(streams, launched):
+        _, res, _ = _decode_result(L, s.cuda_stream)
+        _check(res.status, res)
     return out
 
 
