@@ -39,4 +39,7 @@ for j in jobs:
     print(wl, j.name, "U mean", r[:, 0].mean().round(1), "| PN mean", r[:, 1].mean().round(0), "max", r[:, 1].max(),
           "| sumb", np.bincount(r[:, 2]).tolist(), "| wd", np.bincount(r[:, 3]).tolist(),
           "wc", np.bincount(r[:, 4]).tolist(), "wo", np.bincount(r[:, 5]).tolist())
+    print("  K2s limits: sumb > 4 in %.2f%%, PN > 32768 in %.2f%%, both %.2f%%; PN histogram (2^k)" % (
+        100 * (r[:, 2] > 4).mean(), 100 * (r[:, 1] > 32768).mean(), 100 * ((r[:, 2] > 4) & (r[:, 1] > 32768)).mean()),
+        np.bincount(np.ceil(np.log2(np.maximum(r[:, 1], 1))).astype(int)).tolist())
     print("  paths", gz.pipeline.last_path_counts())
