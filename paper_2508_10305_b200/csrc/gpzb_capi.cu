@@ -270,8 +270,12 @@ void launch_decode(const DecParams& P, bool pres, cudaStream_t s) {
     const int per_sm = occupancy(k_decode_warp<D, F64>, 32 * kWarpDecWarps, kWarpDecSmemBytes);
     const unsigned wgrid = (unsigned)std::min<uint64_t>((nb + kWarpDecWarps - 1) / kWarpDecWarps,
                                                         (uint64_t)sm_count() * per_sm);
+    DecParams Q = P;  // L2 prefetch distance: one claim round of the grid ahead (gpzb_decode_warp.cuh)
+    Q.pf_blks = (uint64_t)GPZB_K4W_PF * wgrid * kWarpDecWarps * warp_claim_chunk((uint32_t)nb, wgrid);
+    const uint64_t avg = P.nblocks ? P.payload_len / P.nblocks : 0;
+    Q.pf_dist = avg >= GPZB_K4W_PF_MIN ? (avg * Q.pf_blks + 15) & ~15ull : 0ull;
     GPZB_COUNT_LAUNCH();
-    k_decode_warp<D, F64><<<wgrid, 32 * kWarpDecWarps, kWarpDecSmemBytes, s>>>(P);
+    k_decode_warp<D, F64><<<wgrid, 32 * kWarpDecWarps, kWarpDecSmemBytes, s>>>(Q);
     GPZB_COUNT_LAUNCH();
     k_decode_list<D, F64, false><<<lgrid, kThreads, 0, s>>>(P, P.list);
   }

@@ -66,6 +66,8 @@ struct DecParams {
   uint32_t* list;          // K4a: blocks for the CTA decoder (count in res->wide_count)
   uint64_t blk_lo, blk_hi; // this launch decodes blocks [blk_lo, blk_hi) (chunked host pipelines)
   uint8_t* big;            // K4b: per-CTA workspace slices (block_size > 1024)
+  uint64_t pf_dist;        // K4w: L2 prefetch distance in payload bytes (0 = off), set at launch
+  uint64_t pf_blks;        // K4w: the same distance in blocks
 };
 
 constexpr int kDecStageWords = 5120;  // 20 KB payload window (legit blocks <= 19.2 KB)
