@@ -175,10 +175,19 @@ CompactParams make_compact(const EncParams& P, int dims, bool f64) {
   return C;
 }
 
-// K3b: table entries, global header, payload moves.
-void launch_emit(const CompactParams& C, cudaStream_t s) {
+// K3b: table entries, global header, payload moves; lanes per block from the
+// average payload when the caller knows it (0: a full warp per block).
+#ifndef GPZB_K3B_G
+#define GPZB_K3B_G 0  // 0: by the average payload; else fixed 8 / 16 / 32
+#endif
+void launch_emit(const CompactParams& C, cudaStream_t s, uint64_t avg_payload = 0) {
+  int g = GPZB_K3B_G ? GPZB_K3B_G : avg_payload == 0 || avg_payload >= 1024 ? 32 : avg_payload >= 384 ? 16 : 8;
+  const uint64_t per_cta = (uint64_t)kCopyWarps * 32 / g;
+  const unsigned grid = (unsigned)((C.nblocks + per_cta - 1) / per_cta);
   GPZB_COUNT_LAUNCH();
-  k_copy_payloads<<<(unsigned)((C.nblocks + kCopyWarps - 1) / kCopyWarps), 32 * kCopyWarps, 0, s>>>(C);
+  if (g == 8) k_copy_payloads<8><<<grid, 32 * kCopyWarps, 0, s>>>(C);
+  else if (g == 16) k_copy_payloads<16><<<grid, 32 * kCopyWarps, 0, s>>>(C);
+  else k_copy_payloads<32><<<grid, 32 * kCopyWarps, 0, s>>>(C);
 }
 
 template <int D, bool F64>
@@ -720,7 +729,9 @@ int gpzb_emit_async(const void* const* axes, int dims, int prec, uint64_t count,
   P.preserve = pres != 0;
   P.side = const_cast<uint8_t*>(side);
   set_out(P, out, nb, table_base, header_count, header_blocks, write_header);
-  launch_emit(make_compact(P, dims, prec == GPZB_F64), (cudaStream_t)stream);
+  // out_cap is the exact container (or this shard's part of it) when the caller sized it from the scan
+  const uint64_t fixed = (write_header ? GPZB_GLOBAL_HEADER_SIZE : 0) + 8 * (nb + 1);
+  launch_emit(make_compact(P, dims, prec == GPZB_F64), (cudaStream_t)stream, out_cap > fixed ? (out_cap - fixed) / nb : 0);
   return cuda_status(cudaGetLastError());
 }
 

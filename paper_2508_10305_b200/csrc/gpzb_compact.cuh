@@ -11,7 +11,7 @@
 //                        tile words): exclusive offsets in place and the
 //                        total payload length (the container size is known
 //                        here, so the caller can allocate it exactly)
-//   K3b k_copy_payloads  one warp per block: its u64 LE offset-table entry,
+//   K3b k_copy_payloads  8-32 lanes per block: its u64 LE offset-table entry,
 //                        and the payload moved from its slot to its byte
 //                        offset (arbitrary alignment) with funnel-shifted
 //                        16-byte stores; edge chunks shared with the
@@ -200,9 +200,14 @@ __device__ __forceinline__ void slot_copy(uint8_t* __restrict__ dst, const uint4
 
 constexpr int kCopyWarps = 8;
 
+// G lanes per block (8, 16 or 32; the host picks it from the average
+// payload): small payloads leave most of a warp idle and every block waits on
+// the same two dependent loads, so a warp moves 32 / G blocks at once.
+template <int G>
 __global__ void __launch_bounds__(32 * kCopyWarps) k_copy_payloads(const CompactParams P) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t blk = (uint64_t)blockIdx.x * kCopyWarps + (threadIdx.x >> 5);
+  static_assert(G == 8 || G == 16 || G == 32, "lanes per block");
+  const int lane = threadIdx.x & (G - 1);
+  const uint64_t blk = (uint64_t)blockIdx.x * (kCopyWarps * 32 / G) + (threadIdx.x / G);
   if (blk >= P.nblocks) return;
   // the scan result and the record's kind are independent loads: both in flight at once
   // (also loading this lane's first slot chunks ahead of the scan result was 1% slower)
@@ -216,7 +221,7 @@ __global__ void __launch_bounds__(32 * kCopyWarps) k_copy_payloads(const Compact
   if (blk == 0 && lane == 2 && P.header) write_global_header(P);
   if (len == 0) return;
   const uint8_t* src = kind == KIND_WIDE ? P.side + P.rec[blk].side_off : P.staging + blk * (uint64_t)kSlotBytes;
-  slot_copy(P.payload + ex, reinterpret_cast<const uint4*>(src), len, lane, 32);
+  slot_copy(P.payload + ex, reinterpret_cast<const uint4*>(src), len, lane, G);
 }
 
 // Diagnostics: how many blocks took each offset-order path (BlkRec::path).

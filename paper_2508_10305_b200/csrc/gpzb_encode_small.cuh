@@ -43,9 +43,6 @@ namespace gpzb {
 #ifndef GPZB_K2S_MINB
 #define GPZB_K2S_MINB 7
 #endif
-#ifndef GPZB_K2S_L2PF
-#define GPZB_K2S_L2PF 0  // L2 bulk prefetch of the block after next
-#endif
 #ifndef GPZB_K2S0_MINB
 #define GPZB_K2S0_MINB 7
 #endif
@@ -168,9 +165,6 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
   // thread 0 keeps the list entry of the block after next in a register, read
   // one block ahead, so issuing the next bulk copy never waits on global memory
   uint32_t next_blk = (tid == 0 && blockIdx.x + gridDim.x < nlist) ? list_at(blockIdx.x + gridDim.x) : 0u;
-#if GPZB_K2S_L2PF
-  uint32_t nn_blk = (tid == 0 && blockIdx.x + 2 * gridDim.x < nlist) ? list_at(blockIdx.x + 2 * gridDim.x) : 0u;
-#endif
   __syncthreads();
 
   const uint32_t bm_s = smem_u32(sm.bm);
@@ -257,22 +251,7 @@ __global__ void __launch_bounds__(kST, HAS_OFF ? GPZB_K2S_MINB : GPZB_K2S0_MINB)
       fence_proxy_async_smem();
       sm.blk = next_blk;
       small_fetch<D, HAS_OFF>(P, sm, next_blk);
-#if GPZB_K2S_L2PF
-      // the block after next into L2 one block ahead of its bulk copy (its
-      // list entry was read one block ago)
-      if (item + 2 * gridDim.x < nlist) {
-        next_blk = nn_blk;
-#pragma unroll
-        for (int a = 0; a < D; ++a)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const float*>(P.axes[a]) +
-                                                                          (uint64_t)nn_blk * kMaxBs),
-                       "r"(kMaxBs * 4)
-                       : "memory");
-        if (item + 3 * gridDim.x < nlist) nn_blk = list_at(item + 3 * gridDim.x);
-      }
-#else
       if (item + 2 * gridDim.x < nlist) next_blk = list_at(item + 2 * gridDim.x);
-#endif
     }
 #pragma unroll
     for (int k = 0; k < kSP; ++k) {
