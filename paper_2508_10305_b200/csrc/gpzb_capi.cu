@@ -38,7 +38,7 @@ std::atomic<unsigned long long> g_launches{0};
 inline uint64_t align_up(uint64_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
 
 struct EncLayout {
-  uint64_t status, tstat, bounds, rec, list, ctalist, slist, staging, big, total;
+  uint64_t status, tstat, bounds, rec, list, ctalist, slist, wlist, staging, big, total;
 };
 constexpr uint32_t kMaxBigBs = 1u << 24;  // K2b / K4b: larger blocks are refused (GPZB_UNSUPPORTED)
 
@@ -59,7 +59,8 @@ EncLayout enc_layout(uint64_t nblocks, int dims, int prec, uint32_t bs = kMaxBs)
   L.list = align_up(L.rec + nblocks * sizeof(BlkRec));
   L.ctalist = align_up(L.list + 4 * nblocks);
   L.slist = align_up(L.ctalist + 4 * nblocks);
-  L.staging = align_up(L.slist + 4 * nblocks);
+  L.wlist = align_up(L.slist + 4 * nblocks);
+  L.staging = align_up(L.wlist + 4 * nblocks);
   // blocks of <= 1024 particles: one staging slot each; larger: K2b's slices
   L.big = align_up(L.staging + (bs <= (uint32_t)kMaxBs ? (uint64_t)kSlotBytes * nblocks : 0));
   L.total = align_up(L.big + (bs > (uint32_t)kMaxBs && nblocks ? big_grid(nblocks, big_enc_slice(bs)) * big_enc_slice(bs) : 0));
@@ -234,10 +235,15 @@ void launch_encode(const EncParams& P, cudaStream_t s) {
     k_encode_small<D, false><<<g0, kST, 0, s>>>(P);
   }
   if (!P.small0 || F64) {
+    // both variants (K1.5's block list / every block in order); the one that
+    // does not match the device-side K2p count exits at once
     const unsigned wgrid = (unsigned)std::min<uint64_t>((P.nblocks + kWarpEncWarps - 1) / kWarpEncWarps,
-                                                        (uint64_t)sm_count() * occupancy(k_encode_warp<D, F64>, 32 * kWarpEncWarps, kWarpEncSmemBytes));
+                                                        (uint64_t)sm_count() * occupancy(k_encode_warp<D, F64, false>, 32 * kWarpEncWarps, kWarpEncSmemBytes));
+    occupancy(k_encode_warp<D, F64, true>, 32 * kWarpEncWarps, kWarpEncSmemBytes);  // sets its shared-memory attribute on this device
     GPZB_COUNT_LAUNCH();
-    k_encode_warp<D, F64><<<wgrid, 32 * kWarpEncWarps, kWarpEncSmemBytes, s>>>(P);
+    k_encode_warp<D, F64, true><<<wgrid, 32 * kWarpEncWarps, kWarpEncSmemBytes, s>>>(P);
+    GPZB_COUNT_LAUNCH();
+    k_encode_warp<D, F64, false><<<wgrid, 32 * kWarpEncWarps, kWarpEncSmemBytes, s>>>(P);
   }
   {
     const unsigned cgrid = (unsigned)std::min<uint64_t>(P.nblocks, (uint64_t)sm_count() * occupancy(k_encode<D, F64>, kThreads, 0));
@@ -363,6 +369,7 @@ EncParams make_enc(const void* const* axes, int dims, int prec, uint64_t count, 
   P.wide_list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + L.list);
   P.cta_list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + L.ctalist);
   P.small_list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + L.slist);
+  P.warp_list = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + L.wlist);
   P.big = static_cast<uint8_t*>(ws) + L.big;
   // routing switches (diagnostics / A-B runs): GPZB_ROUTE=cta sends every
   // narrow block to the general CTA encoder K2, GPZB_ROUTE=small0 sends the

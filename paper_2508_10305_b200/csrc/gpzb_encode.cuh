@@ -45,6 +45,7 @@ struct EncParams {
   uint32_t* wide_list;     // blocks routed to the general encoder
   uint32_t* cta_list;      // narrow blocks for the general CTA encoder K2 (K1.5, then K2s hand-backs)
   uint32_t* small_list;    // K2s blocks: with offsets from the front, offset-free from the back
+  uint32_t* warp_list;     // K2p blocks (K1.5; length res->warp_count)
   uint8_t* big;            // K2b: per-CTA workspace slices (block_size > 1024)
   int small0;              // route offset-free full f32 blocks to K2s (1) or to the warp encoder K2p (0)
   int use_small;           // route blocks to K2s at all (diagnostics switch)
@@ -323,7 +324,6 @@ __global__ void __launch_bounds__(256) k_geometry(const EncParams P) {
         else P.small_list[P.nblocks - 1 - atomicAdd(&R->small0_count, 1u)] = (uint32_t)blk;
       } else if (sumb == 0 && PN <= kWarpEncMaxPN && full) {
         rec.kind = KIND_WARP;
-        atomicAdd(&R->warp_count, 1u);
       } else {
         rec.kind = KIND_NARROW;
         P.cta_list[atomicAdd(&R->cta_count, 1u)] = (uint32_t)blk;
@@ -336,6 +336,17 @@ __global__ void __launch_bounds__(256) k_geometry(const EncParams P) {
       rec.side_off = atomicAdd(&R->side_bytes, (unsigned long long)lb);
       const uint32_t slot = atomicAdd(&R->wide_count, 1u);
       P.wide_list[slot] = (uint32_t)blk;
+    }
+  }
+  {  // K2p's list: one atomic per warp, entries in block order within it
+    const bool isw = rec.kind == KIND_WARP;
+    const unsigned am = __activemask(), m = __ballot_sync(am, isw);
+    if (m) {
+      const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(&R->warp_count, (unsigned)__popc(m));
+      base = __shfl_sync(am, base, leader);
+      if (isw) P.warp_list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)blk;
     }
   }
   reinterpret_cast<BlkRec*>(P.rec)[blk] = rec;

@@ -44,7 +44,7 @@ struct WarpEncSmem {
 };
 constexpr size_t kWarpEncSmemBytes = sizeof(WarpEncSmem) * kWarpEncWarps;
 
-template <int D, bool F64>
+template <int D, bool F64, bool LIST>
 __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_warp(const EncParams P) {
   using T = typename std::conditional<F64, double, float>::type;
   constexpr int S = F64 ? 8 : 4;
@@ -69,22 +69,26 @@ __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_wa
     }
     cp_async_commit();
   };
-  const uint64_t blk0 = (uint64_t)blockIdx.x * kWarpEncWarps + wid;
-  prefetch_rec(blk0, 0);
-  int buf = 0;
-  for (uint64_t blk = blk0; blk < P.nblocks; blk += stride, buf ^= 1) {
+  // LIST (the velocity field: fewer than half the blocks are this kernel's):
+  // K1.5's list of them, entry item + 2 stride read one block ahead of its
+  // use; else every block in order, skipping the others.  Both variants are
+  // launched; the one that does not match the device-side count exits.
+  const uint32_t nlist = *reinterpret_cast<volatile const uint32_t*>(&P.res->warp_count);
+  if ((2ull * nlist < P.nblocks) != LIST) return;
+  // one block: blk, with nxt the block this warp encodes next (>= nblocks: none)
+  auto encode_one = [&](const uint64_t blk, const uint64_t nxt, const int buf) {
     const BlkRec* rec = P.rec + blk;
     cp_async_wait_all();
     __syncwarp();
     const uint32_t* recw = sm.recw[buf];
-    prefetch_rec(blk + stride, buf ^ 1);
-    if ((reinterpret_cast<const uint8_t*>(recw)[offsetof(BlkRec, kind)]) != KIND_WARP) continue;  // warp-uniform
+    prefetch_rec(nxt, buf ^ 1);
+    if ((reinterpret_cast<const uint8_t*>(recw)[offsetof(BlkRec, kind)]) != KIND_WARP) return;  // dense: warp-uniform skip
     const uint64_t first = blk * (uint64_t)P.bs;
 #if GPZB_K2P_L2PF
     // the next block's coordinates into L2 (one bulk prefetch per axis): its
     // loads then wait on L2, not HBM, while this block ranks and packs
-    if (lane < D && blk + GPZB_K2P_L2PF * stride < P.nblocks && P.vec) {
-      const uint64_t nf = (blk + GPZB_K2P_L2PF * stride) * (uint64_t)P.bs;
+    if (lane < D && nxt < P.nblocks && P.vec) {
+      const uint64_t nf = nxt * (uint64_t)P.bs;
       const uint32_t nbytes = (uint32_t)((min((uint64_t)P.bs, P.count - nf) * S) & ~15ull);
       if (nbytes)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const T*>(P.axes[lane]) + nf),
@@ -181,8 +185,8 @@ __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_wa
     }
     // prefetch the next block's chunk 0 (full blocks: always in bounds)
     raw_blk = ~0ull;
-    if (blk + stride < P.nblocks && (blk + stride + 1) * (uint64_t)P.bs <= P.count) {
-      raw_blk = blk + stride;
+    if (nxt < P.nblocks && (nxt + 1) * (uint64_t)P.bs <= P.count) {
+      raw_blk = nxt;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
         const uint4* base = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(P.axes[a]) +
@@ -307,6 +311,21 @@ __global__ void __launch_bounds__(32 * kWarpEncWarps, GPZB_K2P_MINB) k_encode_wa
     uint4* slot = reinterpret_cast<uint4*>(P.staging + blk * (uint64_t)kSlotBytes);
     for (uint32_t w = lane; w < nquads; w += 32) __stcg(slot + w, reinterpret_cast<const uint4*>(st)[w]);
     __syncwarp();  // the next block reuses the shared state
+  };
+  int buf = 0;
+  if constexpr (LIST) {
+    auto entry = [&](uint64_t j) -> uint64_t { return j < nlist ? (uint64_t)P.warp_list[j] : ~0ull; };
+    uint64_t item = (uint64_t)blockIdx.x * kWarpEncWarps + wid;
+    uint64_t blk = entry(item), nxt = entry(item + stride), nn = ~0ull;
+    prefetch_rec(blk, 0);
+    for (; item < nlist; item += stride, buf ^= 1, blk = nxt, nxt = nn) {
+      nn = entry(item + 2 * stride);
+      encode_one(blk, nxt, buf);
+    }
+  } else {
+    const uint64_t blk0 = (uint64_t)blockIdx.x * kWarpEncWarps + wid;
+    prefetch_rec(blk0, 0);
+    for (uint64_t blk = blk0; blk < P.nblocks; blk += stride, buf ^= 1) encode_one(blk, blk + stride, buf);
   }
 }
 
