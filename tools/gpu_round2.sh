@@ -28,7 +28,7 @@ cap() {  # name regex skip [extra bench args]
   ncu -i /tmp/${tag}_$1.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/${tag}_$1_src.csv 2>/dev/null
 }
 cap k2s_vel "^k_encode_small" 2 --compress-only
-cap k2p_pos "^k_encode_warp" 0 --compress-only
+cap k2p_pos "^k_encode_warp" 1 --compress-only  # launch 0 is the list variant of the position call, which exits
 cap k4w_vel "^k_decode_warp" 1
 cap k1_range "^k_range_w" 0 --compress-only
 cap k3b_vel "^k_copy_payloads" 1 --compress-only
