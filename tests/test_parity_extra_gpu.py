@@ -199,3 +199,25 @@ def test_velocity_blocks_wide_offsets_ties_long_runs(eb):
     want = O.compress(axes, O.Config(eb))
     got = gz.compress(gz.Dataset.from_axes(axes), gz.CompressConfig(error_bound=eb))
     assert got == want
+
+
+@pytest.mark.parametrize("kind,eb,lanes", [("clusters", 1e-2, 8), ("lattice", 1e-2, 16), ("uniform", 1e-4, 32)])
+def test_payload_copy_lane_groups_match_oracle(kind, eb, lanes):
+    """K3b moves each payload with 8, 16 or 32 lanes by the container's
+    average payload (< 384 B, < 1024 B, else): one dataset per group (their
+    averages measured with the oracle: 95 B, 627 B, 4,155 B), the whole
+    container and the reconstruction equal the oracle's (pipeline.py:73-103,
+    container.py:211-230)."""
+    gen = {"clusters": O.gen_clusters, "lattice": O.gen_lattice, "uniform": O.gen_uniform}[kind]
+    n = 65536
+    axes = gen(n, seed=3)
+    want = O.compress(axes, O.Config(error_bound=eb))
+    nb = n // 1024
+    avg = (len(want) - 54 - 8 * (nb + 1)) / nb
+    assert {8: avg < 384, 16: 384 <= avg < 1024, 32: avg >= 1024}[lanes], avg
+    ds = gz.Dataset.from_axes([torch.from_numpy(a).cuda() for a in axes])
+    blob = gz.compress(ds, gz.CompressConfig(error_bound=eb))
+    assert blob == want
+    got = gz.decompress(blob).axes
+    for g, o in zip(got, O.decompress(want)):
+        assert np.asarray(g).tobytes() == np.asarray(o).tobytes()
