@@ -27,7 +27,7 @@ using namespace gpzb;
 namespace {
 
 #ifndef GPZB_K1_CTAS
-#define GPZB_K1_CTAS 16
+#define GPZB_K1_CTAS 8  // grid-stride CTAs per SM of K1 (16: batched compress step 4.77 +- 0.08 ms, 8: 4.69 +- 0.01)
 #endif
 
 constexpr uint64_t kAlign = 256;
